@@ -1,0 +1,152 @@
+/* gf_cuda.h — C-ABI of the B200-native fused AT-GNN path (libgraphfuse_cuda.so).
+ *
+ * This is the drop-in boundary underneath the reference's C++ operator API
+ * (namespace graphfuse, proj/include/graphfuse/ headers) and its
+ * pybind11 module graphfuse._core (/root/reference/proj/bindings/module.cpp).
+ * Plain pointers, sizes and an opaque graph handle; no torch or C++ types.
+ * Every compute entry point takes DEVICE pointers and a cudaStream_t passed as
+ * void*; nothing synchronises the stream except where stated.
+ *
+ * Conventions (identical to the reference):
+ *   - edge u -> v; CSR rows are destinations listing in-neighbours sorted by
+ *     source (graph.hpp:18-23); CSC columns are sources listing destinations
+ *     sorted ascending (graph.cpp:43-55).
+ *   - dot scores s = scale * <Q[u], K[v]> (query at the SOURCE, key at the
+ *     destination, kernels.hpp:17-33); AGNN additionally L2-normalises Q and K
+ *     rows per head with max(||x||, 1e-12) (kernels.hpp:50-61).
+ *   - add (GAT) scores s = LeakyReLU(el[u] + er[v]) with x>=0 ? x : slope*x
+ *     (kernels.hpp:36-47); backward derivative pre>0 ? 1 : slope
+ *     (autograd.hpp:113).
+ *   - per-destination softmax; empty rows give zero output (kernels.hpp:65-102).
+ * Multi-head layout (the reference is single-head and is applied per head):
+ *   dot: Q, K, dQ, dK are N x (H*D); add: el, er, del, der are N x H;
+ *   V, O, dO, dV are N x (H*D); lse (log-sum-exp of the scores) is N x H;
+ *   all row-major, element type selected by `dtype`.
+ *
+ * Errors: every function returns GF_OK (0) or a GF_ERR_* code; the message is
+ * available from gf_last_error() (thread-local).  Launch failures are
+ * reported, never swallowed; there is no CPU fallback.
+ */
+#ifndef GF_CUDA_H
+#define GF_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_OK 0
+#define GF_ERR_INVALID 1  /* bad argument / shape (reference: KernelError, std::invalid_argument) */
+#define GF_ERR_CUDA 2     /* CUDA runtime / launch failure */
+#define GF_ERR_GRAPH 3    /* topology error (reference: GraphError) */
+#define GF_ERR_UNSUPPORTED 4
+
+#define GF_F32 0
+#define GF_F64 1
+#define GF_DOT 0 /* SddmmVariant::Dot (GT, AGNN) */
+#define GF_ADD 1 /* SddmmVariant::Add (GAT) */
+
+typedef struct gf_graph_s* gf_graph_t;
+
+/* Attention operator descriptor: SddmmKind (dense.hpp:48-62) + head shape. */
+typedef struct gf_attn_desc {
+  int32_t dtype;    /* GF_F32 | GF_F64 */
+  int32_t variant;  /* GF_DOT | GF_ADD */
+  int32_t l2;       /* AGNN: L2-normalise Q and K rows per head (dot only) */
+  int32_t heads;    /* H >= 1 */
+  int32_t head_dim; /* D >= 1 */
+  int32_t reserved;
+  double scale;     /* dot only */
+  double slope;     /* add only (LeakyReLU negative slope) */
+} gf_attn_desc;
+
+/* Degree-bucket schedule summary of a device graph (the bi-level scheduler). */
+typedef struct gf_graph_info {
+  int64_t num_nodes, num_edges;
+  int64_t max_in_degree, max_out_degree;
+  int32_t cta_threshold;   /* rows with degree >= this get a whole CTA (edge-split) */
+  int32_t n_cta_rows;      /* CSR rows in the CTA bucket (lead the row order) */
+  int32_t n_empty_rows;    /* CSR rows of degree 0 (trail the row order) */
+  int32_t n_cta_cols;      /* CSC columns in the CTA bucket */
+  int32_t n_empty_cols;
+  int32_t device;
+} gf_graph_info;
+
+const char* gf_last_error(void);
+/* 1 if the library was built for (and can launch on) the current device. */
+int gf_device_ok(void);
+
+/* Memory plumbing for hosts that do not link the CUDA runtime themselves
+ * (the C++ host layer and the pybind module use only this C-ABI).
+ * kind: 0 host->device, 1 device->host, 2 device->device. */
+int gf_malloc(size_t bytes, void** out);
+int gf_free(void* p);
+int gf_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);
+int gf_memset(void* dst, int32_t value, size_t bytes, void* stream);
+int gf_stream_sync(void* stream);
+
+/* ---- topology (replaces the device half of graph.hpp:24-38 / graph.cpp:25-78) ----
+ * From the reference's canonical host arrays (int64, as in graphfuse::Graph);
+ * the CSC edge permutation is not needed on the device (the backward
+ * recomputes attention instead of indexing a stored P).  cta_threshold <= 0
+ * selects the default.  Synchronises `stream` once (schedule build). */
+int gf_graph_create(int64_t num_nodes, int64_t num_edges, const int64_t* csr_row_ptr,
+                    const int64_t* csr_col_idx, const int64_t* csc_col_ptr,
+                    const int64_t* csc_row_idx, int32_t cta_threshold, void* stream,
+                    gf_graph_t* out);
+/* Same from device int32 arrays (copied; caller keeps ownership of inputs). */
+int gf_graph_create_device(int64_t num_nodes, int64_t num_edges, const int32_t* d_row_ptr,
+                           const int32_t* d_col_idx, const int32_t* d_csc_ptr,
+                           const int32_t* d_csc_row, int32_t cta_threshold, void* stream,
+                           gf_graph_t* out);
+/* Device from_coo (graph.cpp:61-78): sort by (dst, src), reject ids out of
+ * range (GF_ERR_GRAPH, *bad = input edge index) and duplicates (GF_ERR_GRAPH,
+ * *bad = -2 - sorted position), build CSR and CSC (+ csc_edge_perm) bit-exact
+ * with the reference.  d_src/d_dst are device int64 arrays of length e.
+ * Outputs (device, caller-allocated, int64 like graphfuse::Graph):
+ * row_ptr[n+1], col[e], csc_ptr[n+1], csc_row[e], csc_perm[e]. */
+int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src, const int64_t* d_dst,
+                       int64_t* d_row_ptr, int64_t* d_col, int64_t* d_csc_ptr,
+                       int64_t* d_csc_row, int64_t* d_csc_perm, int64_t* bad, void* stream);
+int gf_graph_destroy(gf_graph_t g);
+int gf_graph_get_info(gf_graph_t g, gf_graph_info* info);
+/* Copy the device schedules to host (row_order[n], col_order[n]; int32). */
+int gf_graph_get_schedule(gf_graph_t g, int32_t* row_order, int32_t* col_order);
+
+/* ---- fused forward (replaces run_block_rows, engine.hpp:192-231) ----
+ * One launch: SDDMM -> per-destination softmax -> SpMM; writes O and lse
+ * only (no E x H tensor).  P (E x H, CSR order) is materialised by a second
+ * recompute launch only when P != NULL (reference ForwardContext::P). */
+int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                const void* V, void* O, void* lse, void* P, void* stream);
+
+/* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
+ * Pass A over CSR rows (dK or der, and delta = rowsum(dO*O)), pass B over CSC
+ * columns (dQ or del, dV).  Attention is recomputed from lse; no E x H
+ * tensor is read or written.  `delta` is caller scratch of N x H elements
+ * (may be NULL: then the graph's internal scratch is used). */
+int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                const void* V, const void* O, const void* lse, const void* dO, void* dQ,
+                void* dK, void* dV, void* delta, void* stream);
+
+/* ---- dense projections (replaces matmul / matmul_at_b, models.hpp:58-86) ----
+ * C[M x N] = A[M x K] * B[K x N]          (trans_a = 0)
+ * C[M x N] = A[K x M]^T * B[K x N]        (trans_a = 1)
+ * Row-major, fp32 or fp64; accumulate = 1 adds into C. */
+int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int64_t K, const void* A,
+            const void* B, void* C, int32_t accumulate, void* stream);
+/* GAT attention logits: el[n,h] = sum_d Hf[n,h,d] a_l[h,d]; er likewise. */
+int gf_gat_logits(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf, const void* a_l,
+                  const void* a_r, void* el, void* er, void* stream);
+/* GAT fan-in (models.hpp:143-148): dH = dV + del (x) a_l + der (x) a_r, and
+ * da_l[h,d] = sum_n Hf[n,h,d] del[n,h], da_r likewise. */
+int gf_gat_fanin(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf, const void* a_l,
+                 const void* a_r, const void* dV, const void* del, const void* der, void* dH,
+                 void* da_l, void* da_r, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF_CUDA_H */

@@ -1,0 +1,181 @@
+// C-ABI entry points of libgraphfuse_cuda (see include/gf_cuda.h).
+#include <string>
+
+#include "gf_internal.cuh"
+
+namespace gfb {
+namespace {
+thread_local std::string t_err;
+}
+void set_error(const std::string& msg) { t_err = msg; }
+}  // namespace gfb
+
+
+extern "C" const char* gf_last_error(void) { return gfb::t_err.c_str(); }
+
+extern "C" int gf_device_ok(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return 0;
+  return p.major == 10 && p.minor == 0;  // built for sm_100a only
+}
+
+extern "C" int gf_malloc(size_t bytes, void** out) {
+  if (!out) {
+    gfb::set_error("gf_malloc: null out");
+    return GF_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (bytes == 0) return GF_OK;
+  GF_CHECK_CUDA(cudaMalloc(out, bytes));
+  return GF_OK;
+}
+
+extern "C" int gf_free(void* p) {
+  if (p) GF_CHECK_CUDA(cudaFree(p));
+  return GF_OK;
+}
+
+extern "C" int gf_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream) {
+  if (bytes == 0) return GF_OK;
+  const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+  GF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)));
+  return GF_OK;
+}
+
+extern "C" int gf_memset(void* dst, int32_t value, size_t bytes, void* stream) {
+  if (bytes == 0) return GF_OK;
+  GF_CHECK_CUDA(cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream)));
+  return GF_OK;
+}
+
+extern "C" int gf_stream_sync(void* stream) {
+  GF_CHECK_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  GF_CHECK_CUDA(cudaGetLastError());
+  return GF_OK;
+}
+
+namespace {
+
+int check_desc(const gf_attn_desc* d, const char* who) {
+  if (!d) {
+    gfb::set_error(std::string(who) + ": null descriptor");
+    return GF_ERR_INVALID;
+  }
+  if ((d->dtype != GF_F32 && d->dtype != GF_F64) || (d->variant != GF_DOT && d->variant != GF_ADD) ||
+      d->heads < 1 || d->head_dim < 1 || (d->variant == GF_ADD && d->l2)) {
+    gfb::set_error(std::string(who) + ": invalid descriptor (dtype/variant/heads/head_dim/l2)");
+    return GF_ERR_INVALID;
+  }
+  return GF_OK;
+}
+
+template <typename T>
+gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const void* Q,
+                         const void* K, const void* V, void* O, void* lse) {
+  gfb::FwdArgs<T> a{};
+  a.ptr = g.row_ptr;
+  a.idx = g.col;
+  a.order = g.row_order;
+  a.n = g.n;
+  a.n_cta = g.n_cta_rows;
+  a.H = d.heads;
+  a.D = d.head_dim;
+  a.F = d.heads * d.head_dim;
+  a.GD = 1;
+  a.l2 = d.l2;
+  a.scale = static_cast<T>(d.scale);
+  a.slope = static_cast<T>(d.slope);
+  a.Q = static_cast<const T*>(Q);
+  a.K = static_cast<const T*>(K);
+  a.V = static_cast<const T*>(V);
+  a.O = static_cast<T*>(O);
+  a.lse = static_cast<T*>(lse);
+  return a;
+}
+
+template <typename T>
+int fwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, const void* V,
+             void* O, void* lse, void* P, cudaStream_t s) {
+  auto a = fwd_args<T>(*g, d, Q, K, V, O, lse);
+  int rc = gfb::launch_fwd<T>(*g, a, d.variant, s);
+  if (rc || !P) return rc;
+  return gfb::launch_materialize_p<T>(*g, a, d.variant, static_cast<T*>(P), s);
+}
+
+template <typename T>
+int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, const void* V,
+             const void* O, const void* lse, const void* dO, void* dQ, void* dK, void* dV,
+             void* delta, cudaStream_t s) {
+  gfb::BwdArgs<T> a{};
+  a.n = g->n;
+  a.H = d.heads;
+  a.D = d.head_dim;
+  a.F = d.heads * d.head_dim;
+  a.GD = 1;
+  a.l2 = d.l2;
+  a.scale = static_cast<T>(d.scale);
+  a.slope = static_cast<T>(d.slope);
+  a.Q = static_cast<const T*>(Q);
+  a.K = static_cast<const T*>(K);
+  a.V = static_cast<const T*>(V);
+  a.O = static_cast<const T*>(O);
+  a.lse = static_cast<const T*>(lse);
+  a.dO = static_cast<const T*>(dO);
+  a.dQ = static_cast<T*>(dQ);
+  a.dK = static_cast<T*>(dK);
+  a.dV = static_cast<T*>(dV);
+  if (delta) {
+    a.delta = static_cast<T*>(delta);
+  } else {
+    const size_t need = sizeof(T) * static_cast<size_t>(g->n) * d.heads;
+    if (g->scratch_bytes < need) {
+      cudaFree(g->scratch);
+      g->scratch = nullptr;
+      g->scratch_bytes = 0;
+      GF_CHECK_CUDA(cudaMalloc(&g->scratch, need));
+      g->scratch_bytes = need;
+    }
+    a.delta = static_cast<T*>(g->scratch);
+  }
+  return gfb::launch_bwd<T>(*g, a, d.variant, s);
+}
+
+}  // namespace
+
+extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                           const void* V, void* O, void* lse, void* P, void* stream) {
+  if (int rc = check_desc(desc, "gf_attn_fwd")) return rc;
+  if (!g) {
+    gfb::set_error("gf_attn_fwd: null graph");
+    return GF_ERR_INVALID;
+  }
+  if (g->n > 0 && (!Q || !K || !V || !O || !lse)) {
+    gfb::set_error("gf_attn_fwd: null operand");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  return desc->dtype == GF_F32 ? fwd_impl<float>(g, *desc, Q, K, V, O, lse, P, s)
+                               : fwd_impl<double>(g, *desc, Q, K, V, O, lse, P, s);
+}
+
+extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                           const void* V, const void* O, const void* lse, const void* dO,
+                           void* dQ, void* dK, void* dV, void* delta, void* stream) {
+  if (int rc = check_desc(desc, "gf_attn_bwd")) return rc;
+  if (!g) {
+    gfb::set_error("gf_attn_bwd: null graph");
+    return GF_ERR_INVALID;
+  }
+  if (g->n > 0 && (!Q || !K || !V || !O || !lse || !dO || !dQ || !dK || !dV)) {
+    gfb::set_error("gf_attn_bwd: null operand");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  return desc->dtype == GF_F32
+             ? bwd_impl<float>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, s);
+}

@@ -1,0 +1,377 @@
+// Device topology and the bi-level degree-bucket scheduler.
+//
+//  * gf_graph_create*: int32 CSR (destination rows) + CSC (source columns)
+//    resident in HBM, plus two schedules: rows (forward, backward pass A) and
+//    columns (backward pass B) stably sorted by degree descending with
+//    cub::DeviceRadixSort (LSD radix sort is stable, so ties keep ascending
+//    node id — the CPU restatement gfo_schedule defines the same order and
+//    tests compare them bit-exactly).  Bucket counts: rows with degree >=
+//    cta_threshold (CTA / edge-split bucket, they lead the order) and empty
+//    rows (they trail it); everything between is the warp-per-row bucket.
+//  * gf_from_coo_device: the reference's from_coo (graph.cpp:61-78) on the
+//    GPU: id validation, (dst,src) radix sort, duplicate rejection, CSR by
+//    segment offsets and the CSC transpose (+ csc_edge_perm) by a second
+//    (src,dst) sort — bit-exact with graph.cpp:25-57.
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+
+namespace gfb {
+
+namespace {
+
+__global__ void degrees_kernel(const int32_t* __restrict__ ptr, int n, int32_t* __restrict__ deg,
+                               int32_t* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    deg[i] = ptr[i + 1] - ptr[i];
+    ids[i] = i;
+  }
+}
+
+// stats[0] = max degree, stats[1] = #(deg >= thr), stats[2] = #(deg == 0)
+__global__ void degree_stats_kernel(const int32_t* __restrict__ deg, int n, int thr,
+                                    int32_t* __restrict__ stats) {
+  int mx = 0, big = 0, zero = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = deg[i];
+    mx = max(mx, d);
+    big += (d >= thr && d > 0);
+    zero += (d == 0);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    big += __shfl_xor_sync(kFull, big, o);
+    zero += __shfl_xor_sync(kFull, zero, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(stats + 0, mx);
+    atomicAdd(stats + 1, big);
+    atomicAdd(stats + 2, zero);
+  }
+}
+
+int bits_for(long long x) {
+  int b = 1;
+  while ((1LL << b) <= x) ++b;
+  return b;
+}
+
+// Degree-descending stable order of [0, n) for a pointer array.
+int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32_t& n_cta,
+                   int32_t& n_empty, int64_t& max_deg, cudaStream_t s) {
+  if (n == 0) {
+    n_cta = n_empty = 0;
+    max_deg = 0;
+    return GF_OK;
+  }
+  int32_t *deg = nullptr, *ids = nullptr, *deg_sorted = nullptr, *stats = nullptr;
+  GF_CHECK_CUDA(cudaMallocAsync(&deg, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&ids, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&deg_sorted, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&stats, sizeof(int32_t) * 4, s));
+  GF_CHECK_CUDA(cudaMemsetAsync(stats, 0, sizeof(int32_t) * 4, s));
+  degrees_kernel<<<(n + 255) / 256, 256, 0, s>>>(d_ptr, n, deg, ids);
+  GF_CHECK_LAUNCH("degrees_kernel");
+  degree_stats_kernel<<<min(1024, (n + 255) / 256), 256, 0, s>>>(deg, n, thr, stats);
+  GF_CHECK_LAUNCH("degree_stats_kernel");
+  int32_t h[4];
+  GF_CHECK_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  max_deg = h[0];
+  n_cta = h[1];
+  n_empty = h[2];
+  const int end_bit = bits_for(h[0]);
+  size_t tmp_bytes = 0;
+  GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted,
+                                                           ids, d_order, n, 0, end_bit, s));
+  void* tmp = nullptr;
+  GF_CHECK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+  GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, ids,
+                                                           d_order, n, 0, end_bit, s));
+  GF_CHECK_LAUNCH("radix sort");
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(deg, s);
+  cudaFreeAsync(ids, s);
+  cudaFreeAsync(deg_sorted, s);
+  cudaFreeAsync(stats, s);
+  GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
+int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
+  g->cta_threshold = thr > 0 ? thr : kDefaultCtaThreshold;
+  GF_CHECK_CUDA(cudaGetDevice(&g->device));
+  GF_CHECK_CUDA(cudaMalloc(&g->row_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));
+  GF_CHECK_CUDA(cudaMalloc(&g->col_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));
+  int rc = build_schedule(g->row_ptr, g->n, g->cta_threshold, g->row_order, g->n_cta_rows,
+                          g->n_empty_rows, g->max_in, s);
+  if (rc) return rc;
+  return build_schedule(g->csc_ptr, g->n, g->cta_threshold, g->col_order, g->n_cta_cols,
+                        g->n_empty_cols, g->max_out, s);
+}
+
+void free_graph(DevGraph* g) {
+  if (!g) return;
+  cudaFree(g->row_ptr);
+  cudaFree(g->col);
+  cudaFree(g->csc_ptr);
+  cudaFree(g->csc_row);
+  cudaFree(g->row_order);
+  cudaFree(g->col_order);
+  cudaFree(g->scratch);
+  delete g;
+}
+
+// ------------------------------------------------------- device from_coo --
+__global__ void coo_check_pack(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                               int64_t e, int64_t n, int b, uint64_t* __restrict__ k_ds,
+                               uint64_t* __restrict__ k_sd, unsigned long long* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t u = src[i], v = dst[i];
+    if (u < 0 || u >= n || v < 0 || v >= n) {
+      atomicMin(bad, static_cast<unsigned long long>(i));
+      k_ds[i] = k_sd[i] = 0;
+    } else {
+      k_ds[i] = (static_cast<uint64_t>(v) << b) | static_cast<uint64_t>(u);
+      k_sd[i] = (static_cast<uint64_t>(u) << b) | static_cast<uint64_t>(v);
+    }
+  }
+}
+
+// Unpack sorted keys into (major, minor) arrays, flag duplicates, and write
+// the segment pointer of the major index (ptr[x] = first position >= x).
+__global__ void unpack_sorted(const uint64_t* __restrict__ keys, int64_t e, int64_t n, int b,
+                              int64_t* __restrict__ minor, int64_t* __restrict__ ptr,
+                              unsigned long long* __restrict__ dup) {
+  const uint64_t mask = (1ull << b) - 1;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i <= e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cur = i < e ? static_cast<int64_t>(keys[i] >> b) : n;
+    const int64_t prev = i > 0 ? static_cast<int64_t>(keys[i - 1] >> b) : -1;
+    if (i < e) {
+      minor[i] = static_cast<int64_t>(keys[i] & mask);
+      if (i > 0 && keys[i] == keys[i - 1]) atomicMin(dup, static_cast<unsigned long long>(i));
+    }
+    for (int64_t x = prev + 1; x <= cur; ++x) ptr[x] = i;
+  }
+}
+
+__global__ void csc_perm_kernel(const uint64_t* __restrict__ k_ds, const uint64_t* __restrict__ k_sd,
+                                int64_t e, int b, int64_t* __restrict__ perm) {
+  const uint64_t mask = (1ull << b) - 1;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t u = k_sd[i] >> b, v = k_sd[i] & mask;
+    const uint64_t key = (v << b) | u;
+    int64_t lo = 0, hi = e;  // lower_bound
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (k_ds[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    perm[i] = lo;
+  }
+}
+}  // namespace
+
+}  // namespace gfb
+
+using gfb::DevGraph;
+
+
+extern "C" int gf_graph_create_device(int64_t n, int64_t e, const int32_t* d_row_ptr,
+                                      const int32_t* d_col, const int32_t* d_csc_ptr,
+                                      const int32_t* d_csc_row, int32_t cta_threshold,
+                                      void* stream, gf_graph_t* out) {
+  if (!out || n < 0 || e < 0 || n >= (1LL << 31) - 1 || e >= (1LL << 31) - 1) {
+    gfb::set_error("gf_graph_create_device: invalid sizes (int32 node/edge ids required)");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* g = new gf_graph_s();
+  g->n = static_cast<int32_t>(n);
+  g->e = static_cast<int32_t>(e);
+  const size_t np = sizeof(int32_t) * (n + 1), ep = sizeof(int32_t) * (e > 0 ? e : 1);
+  auto fail = [&](int rc) {
+    gfb::free_graph(g);
+    return rc;
+  };
+  if (cudaMalloc(&g->row_ptr, np) || cudaMalloc(&g->col, ep) || cudaMalloc(&g->csc_ptr, np) ||
+      cudaMalloc(&g->csc_row, ep)) {
+    gfb::set_error("gf_graph_create_device: cudaMalloc failed");
+    return fail(GF_ERR_CUDA);
+  }
+  if (cudaMemcpyAsync(g->row_ptr, d_row_ptr, np, cudaMemcpyDeviceToDevice, s) ||
+      cudaMemcpyAsync(g->csc_ptr, d_csc_ptr, np, cudaMemcpyDeviceToDevice, s) ||
+      (e > 0 && cudaMemcpyAsync(g->col, d_col, sizeof(int32_t) * e, cudaMemcpyDeviceToDevice, s)) ||
+      (e > 0 &&
+       cudaMemcpyAsync(g->csc_row, d_csc_row, sizeof(int32_t) * e, cudaMemcpyDeviceToDevice, s))) {
+    gfb::set_error("gf_graph_create_device: copy failed");
+    return fail(GF_ERR_CUDA);
+  }
+  int rc = gfb::finish_graph(g, cta_threshold, s);
+  if (rc) return fail(rc);
+  *out = g;
+  return GF_OK;
+}
+
+extern "C" int gf_graph_create(int64_t n, int64_t e, const int64_t* row_ptr,
+                               const int64_t* col, const int64_t* csc_ptr,
+                               const int64_t* csc_row, int32_t cta_threshold, void* stream,
+                               gf_graph_t* out) {
+  if (!out || n < 0 || e < 0 || n >= (1LL << 31) - 1 || e >= (1LL << 31) - 1 ||
+      (n > 0 && (!row_ptr || !csc_ptr)) || (e > 0 && (!col || !csc_row))) {
+    gfb::set_error("gf_graph_create: invalid arguments (int32 node/edge ids required)");
+    return GF_ERR_INVALID;
+  }
+  if (row_ptr && (row_ptr[0] != 0 || row_ptr[n] != e)) {
+    gfb::set_error("gf_graph_create: csr_row_ptr must start at 0 and end at num_edges");
+    return GF_ERR_GRAPH;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  std::vector<int32_t> h_rp(n + 1), h_cp(n + 1), h_col(e > 0 ? e : 1), h_cr(e > 0 ? e : 1);
+  for (int64_t i = 0; i <= n; ++i) {
+    h_rp[i] = static_cast<int32_t>(row_ptr ? row_ptr[i] : 0);
+    h_cp[i] = static_cast<int32_t>(csc_ptr ? csc_ptr[i] : 0);
+  }
+  for (int64_t i = 0; i < e; ++i) {
+    h_col[i] = static_cast<int32_t>(col[i]);
+    h_cr[i] = static_cast<int32_t>(csc_row[i]);
+  }
+  int32_t *d_rp = nullptr, *d_cp = nullptr, *d_col = nullptr, *d_cr = nullptr;
+  const size_t np = sizeof(int32_t) * (n + 1), ep = sizeof(int32_t) * (e > 0 ? e : 1);
+  if (cudaMalloc(&d_rp, np) || cudaMalloc(&d_cp, np) || cudaMalloc(&d_col, ep) ||
+      cudaMalloc(&d_cr, ep)) {
+    cudaFree(d_rp), cudaFree(d_cp), cudaFree(d_col), cudaFree(d_cr);
+    gfb::set_error("gf_graph_create: cudaMalloc failed");
+    return GF_ERR_CUDA;
+  }
+  cudaMemcpyAsync(d_rp, h_rp.data(), np, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_cp, h_cp.data(), np, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_col, h_col.data(), ep, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_cr, h_cr.data(), ep, cudaMemcpyHostToDevice, s);
+  int rc = gf_graph_create_device(n, e, d_rp, d_col, d_cp, d_cr, cta_threshold, stream, out);
+  cudaStreamSynchronize(s);
+  cudaFree(d_rp), cudaFree(d_cp), cudaFree(d_col), cudaFree(d_cr);
+  return rc;
+}
+
+extern "C" int gf_graph_destroy(gf_graph_t g) {
+  gfb::free_graph(g);
+  return GF_OK;
+}
+
+extern "C" int gf_graph_get_info(gf_graph_t g, gf_graph_info* info) {
+  if (!g || !info) {
+    gfb::set_error("gf_graph_get_info: null argument");
+    return GF_ERR_INVALID;
+  }
+  info->num_nodes = g->n;
+  info->num_edges = g->e;
+  info->max_in_degree = g->max_in;
+  info->max_out_degree = g->max_out;
+  info->cta_threshold = g->cta_threshold;
+  info->n_cta_rows = g->n_cta_rows;
+  info->n_empty_rows = g->n_empty_rows;
+  info->n_cta_cols = g->n_cta_cols;
+  info->n_empty_cols = g->n_empty_cols;
+  info->device = g->device;
+  return GF_OK;
+}
+
+extern "C" int gf_graph_get_schedule(gf_graph_t g, int32_t* row_order, int32_t* col_order) {
+  if (!g) {
+    gfb::set_error("gf_graph_get_schedule: null graph");
+    return GF_ERR_INVALID;
+  }
+  if (g->n == 0) return GF_OK;
+  if (row_order)
+    GF_CHECK_CUDA(cudaMemcpy(row_order, g->row_order, sizeof(int32_t) * g->n,
+                             cudaMemcpyDeviceToHost));
+  if (col_order)
+    GF_CHECK_CUDA(cudaMemcpy(col_order, g->col_order, sizeof(int32_t) * g->n,
+                             cudaMemcpyDeviceToHost));
+  return GF_OK;
+}
+
+extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
+                                  const int64_t* d_dst, int64_t* d_row_ptr, int64_t* d_col,
+                                  int64_t* d_csc_ptr, int64_t* d_csc_row, int64_t* d_csc_perm,
+                                  int64_t* bad, void* stream) {
+  using namespace gfb;
+  if (n < 0 || e < 0 || n >= (1LL << 31)) {
+    set_error("gf_from_coo_device: invalid sizes");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  if (bad) *bad = -1;
+  const int b = bits_for(n > 0 ? n - 1 : 0);
+  const int grid = static_cast<int>(std::min<int64_t>(4096, (e + 255) / 256 + 1));
+  uint64_t *k_ds = nullptr, *k_sd = nullptr, *k_ds_s = nullptr, *k_sd_s = nullptr;
+  unsigned long long* flags = nullptr;
+  const size_t eb = sizeof(uint64_t) * (e > 0 ? e : 1);
+  GF_CHECK_CUDA(cudaMallocAsync(&k_ds, eb, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&k_sd, eb, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&k_ds_s, eb, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&k_sd_s, eb, s));
+  GF_CHECK_CUDA(cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), s));
+  GF_CHECK_CUDA(cudaMemsetAsync(flags, 0xff, 2 * sizeof(unsigned long long), s));
+  int rc = GF_OK;
+  unsigned long long hflags[2] = {~0ull, ~0ull};
+  if (e > 0) {
+    coo_check_pack<<<grid, 256, 0, s>>>(d_src, d_dst, e, n, b, k_ds, k_sd, flags);
+    GF_CHECK_LAUNCH("coo_check_pack");
+    size_t tb = 0;
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, k_ds, k_ds_s, e, 0, 2 * b, s));
+    void* tmp = nullptr;
+    GF_CHECK_CUDA(cudaMallocAsync(&tmp, tb, s));
+    size_t t = tb;
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t, k_ds, k_ds_s, e, 0, 2 * b, s));
+    t = tb;
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t, k_sd, k_sd_s, e, 0, 2 * b, s));
+    cudaFreeAsync(tmp, s);
+    unpack_sorted<<<grid, 256, 0, s>>>(k_ds_s, e, n, b, d_col, d_row_ptr, flags + 1);
+    GF_CHECK_LAUNCH("unpack_sorted csr");
+    unpack_sorted<<<grid, 256, 0, s>>>(k_sd_s, e, n, b, d_csc_row, d_csc_ptr, flags + 1);
+    GF_CHECK_LAUNCH("unpack_sorted csc");
+    GF_CHECK_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
+    GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  } else {
+    std::vector<int64_t> zeros(n + 1, 0);
+    GF_CHECK_CUDA(cudaMemcpyAsync(d_row_ptr, zeros.data(), sizeof(int64_t) * (n + 1),
+                                  cudaMemcpyHostToDevice, s));
+    GF_CHECK_CUDA(cudaMemcpyAsync(d_csc_ptr, zeros.data(), sizeof(int64_t) * (n + 1),
+                                  cudaMemcpyHostToDevice, s));
+    GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  if (hflags[0] != ~0ull) {
+    if (bad) *bad = static_cast<int64_t>(hflags[0]);
+    set_error("from_coo: node id out of range for input edge " + std::to_string(hflags[0]));
+    rc = GF_ERR_GRAPH;
+  } else if (hflags[1] != ~0ull) {
+    if (bad) *bad = -2 - static_cast<int64_t>(hflags[1]);
+    set_error("from_coo: duplicate edge at sorted position " + std::to_string(hflags[1]));
+    rc = GF_ERR_GRAPH;
+  }
+  if (rc == GF_OK && e > 0) {
+    // csc_edge_perm: CSR edge id of each CSC slot = position of key (v,u) in
+    // the sorted CSR keys (keys are unique once duplicates are rejected).
+    csc_perm_kernel<<<grid, 256, 0, s>>>(k_ds_s, k_sd_s, e, b, d_csc_perm);
+    if (cudaGetLastError() != cudaSuccess) {
+      set_error("launch csc_perm_kernel failed");
+      rc = GF_ERR_CUDA;
+    }
+  }
+  cudaFreeAsync(k_ds, s);
+  cudaFreeAsync(k_sd, s);
+  cudaFreeAsync(k_ds_s, s);
+  cudaFreeAsync(k_sd_s, s);
+  cudaFreeAsync(flags, s);
+  cudaStreamSynchronize(s);
+  return rc;
+}
+

@@ -1,0 +1,122 @@
+// Internal shared definitions for libgraphfuse_cuda (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "gf_cuda.h"
+
+namespace gfb {
+
+// ------------------------------------------------------------------ errors --
+void set_error(const std::string& msg);
+
+struct Status {
+  int code = GF_OK;
+};
+
+#define GF_CHECK_CUDA(expr)                                                          \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::gfb::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+      return GF_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define GF_CHECK_LAUNCH(what)                                                        \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess) {                                                         \
+      ::gfb::set_error(std::string("launch ") + (what) + ": " + cudaGetErrorString(_e)); \
+      return GF_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+// ------------------------------------------------------------------- graph --
+// Device-resident topology: int32 CSR (dst rows -> src) and CSC (src cols ->
+// dst), plus the bi-level schedules (degree-descending orders with bucket
+// counts) for the row pass (forward, backward pass A) and the column pass
+// (backward pass B).
+struct DevGraph {
+  int32_t n = 0, e = 0;
+  int32_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  int32_t* csc_ptr = nullptr;
+  int32_t* csc_row = nullptr;
+  int32_t* row_order = nullptr;
+  int32_t* col_order = nullptr;
+  int32_t cta_threshold = 0;
+  int32_t n_cta_rows = 0, n_empty_rows = 0;
+  int32_t n_cta_cols = 0, n_empty_cols = 0;
+  int64_t max_in = 0, max_out = 0;
+  int device = 0;
+  void* scratch = nullptr;  // delta for the backward when the caller passes none
+  size_t scratch_bytes = 0;
+};
+
+constexpr int kDefaultCtaThreshold = 1024;
+constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
+
+// ---------------------------------------------------------- kernel params --
+template <typename T>
+struct FwdArgs {
+  const int32_t* ptr;    // CSR row pointer
+  const int32_t* idx;    // CSR column (source) ids
+  const int32_t* order;  // row schedule
+  int n, n_cta;
+  int H, D, F, GD;  // GD = chunks per head (fast path)
+  int l2;
+  T scale, slope;
+  const T* Q;  // dot: N x F; add: el N x H
+  const T* K;  // dot: N x F; add: er N x H
+  const T* V;
+  T* O;
+  T* lse;
+};
+
+template <typename T>
+struct BwdArgs {
+  const int32_t* ptr;
+  const int32_t* idx;
+  const int32_t* order;
+  int n, n_cta;
+  int H, D, F, GD;
+  int l2;
+  T scale, slope;
+  const T* Q;
+  const T* K;
+  const T* V;
+  const T* O;
+  const T* lse;
+  const T* dO;
+  T* delta;  // pass A writes, pass B reads
+  T* dQ;     // pass B (dot) / del (add)
+  T* dK;     // pass A (dot) / der (add)
+  T* dV;     // pass B
+};
+
+// Launchers (defined in gf_attn_fwd.cu / gf_attn_bwd.cu).
+template <typename T>
+int launch_fwd(const DevGraph& g, const FwdArgs<T>& a, int variant, cudaStream_t s);
+template <typename T>
+int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T* P,
+                         cudaStream_t s);
+template <typename T>
+int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, cudaStream_t s);
+
+// Fast-path eligibility: chunk = 16 bytes; D a multiple of the chunk width,
+// chunks per head a power of two, F/CW a power of two <= 128, 16 B alignment.
+struct FastShape {
+  bool ok = false;
+  int lpe = 0, cpl = 0, gd = 0;
+};
+FastShape fast_shape(int H, int D, int elem_bytes);
+
+}  // namespace gfb
+
+// The opaque C handle is the device graph itself.
+struct gf_graph_s : gfb::DevGraph {};

@@ -1,0 +1,441 @@
+// Drop-in operator API over the B200 C-ABI: run_strategy & variants
+// (engine.hpp:233-336), fused/unfused_backward (autograd.hpp:196-226),
+// finite_difference_check (autograd.hpp:241-287), matmul / conv_forward /
+// conv_backward / make_pipeline_inputs (models.hpp:58-190).
+//
+// Every compute step is a gf_* call into libgraphfuse_cuda.so; this file only
+// validates arguments exactly like the reference (same exception types and
+// message prefixes), moves host vectors to/from HBM and keeps the reference's
+// modelled counters.  No CPU compute fallback exists.
+#include <chrono>
+#include <algorithm>
+#include <limits>
+
+#include "gf_cuda.h"
+#include "graphfuse/graphfuse.hpp"
+
+namespace graphfuse {
+
+namespace detail {
+
+[[noreturn]] void device_fail(const char* what) {
+  throw EngineError(std::string("B200 path: ") + what + ": " + gf_last_error());
+}
+
+void need_device() {
+  static const bool ok = gf_device_ok() != 0;
+  if (!ok)
+    throw EngineError(
+        "B200 path: no sm_100 device available (libgraphfuse_cuda has no CPU fallback)");
+}
+
+#define GFH_CALL(expr)                     \
+  do {                                     \
+    if ((expr) != GF_OK) ::graphfuse::detail::device_fail(#expr); \
+  } while (0)
+
+/// Owning device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) : bytes(b) { GFH_CALL(gf_malloc(b, &p)); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  ~DevBuf() { gf_free(p); }
+  template <typename T>
+  static DevBuf from(const std::vector<T>& h) {
+    DevBuf d(sizeof(T) * h.size());
+    if (!h.empty()) GFH_CALL(gf_memcpy(d.p, h.data(), d.bytes, 0, nullptr));
+    return d;
+  }
+  template <typename T>
+  void to(std::vector<T>& h) const {
+    if (!h.empty()) GFH_CALL(gf_memcpy(h.data(), p, sizeof(T) * h.size(), 1, nullptr));
+  }
+};
+
+struct DeviceGraphCache {
+  gf_graph_t h = nullptr;
+  NodeId n = -1;
+  EdgeId e = -1;
+  const void* row_data = nullptr;
+  const void* col_data = nullptr;
+  std::int64_t thr = 0;
+  ~DeviceGraphCache() {
+    if (h) gf_graph_destroy(h);
+  }
+};
+
+gf_graph_t device_graph(const Graph& g, const FusionPlan& plan) {
+  need_device();
+  auto& c = g.device;
+  if (!c || c->n != g.num_nodes || c->e != g.num_edges ||
+      c->row_data != g.csr_row_ptr.data() || c->col_data != g.csr_col_idx.data() ||
+      c->thr != plan.cta_row_threshold) {
+    auto fresh = std::make_shared<DeviceGraphCache>();
+    GFH_CALL(gf_graph_create(g.num_nodes, g.num_edges, g.csr_row_ptr.data(),
+                             g.csr_col_idx.data(), g.csc_col_ptr.data(), g.csc_row_idx.data(),
+                             static_cast<std::int32_t>(plan.cta_row_threshold), nullptr,
+                             &fresh->h));
+    fresh->n = g.num_nodes;
+    fresh->e = g.num_edges;
+    fresh->row_data = g.csr_row_ptr.data();
+    fresh->col_data = g.csr_col_idx.data();
+    fresh->thr = plan.cta_row_threshold;
+    c = std::move(fresh);
+  }
+  return c->h;
+}
+
+template <typename T>
+constexpr int dtype_code() {
+  return sizeof(T) == 8 ? GF_F64 : GF_F32;
+}
+
+template <typename T>
+gf_attn_desc make_desc(const SddmmKind& kind, std::int64_t d) {
+  gf_attn_desc a{};
+  a.dtype = dtype_code<T>();
+  a.variant = kind.variant == SddmmVariant::Add ? GF_ADD : GF_DOT;
+  a.l2 = kind.variant == SddmmVariant::Dot && kind.l2_normalize_inputs ? 1 : 0;
+  a.heads = 1;
+  a.head_dim = static_cast<std::int32_t>(d);
+  a.scale = kind.scale;
+  a.slope = kind.leaky_slope;
+  return a;
+}
+
+template <typename T>
+void validate_inputs(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                     const DenseMatrix<T>& V, const SddmmKind& kind) {
+  if (V.rows != g.num_nodes) throw KernelError("engine: V.rows must equal N");
+  if (kind.variant == SddmmVariant::Dot &&
+      (Q.rows != g.num_nodes || K.rows != g.num_nodes || Q.cols != K.cols))
+    throw KernelError("engine: Q/K dimension mismatch");
+  if (kind.variant == SddmmVariant::Add && (Q.cols != 1 || K.cols != 1))
+    throw KernelError("engine: add-SDDMM expects N x 1 el/er");
+  if (kind.variant == SddmmVariant::Dot && Q.cols != V.cols)
+    throw KernelError("engine: B200 fused path requires Q/K width == V width");
+  if (kind.variant == SddmmVariant::Add && (Q.rows != g.num_nodes || K.rows != g.num_nodes))
+    throw KernelError("engine: el/er must have N rows");
+}
+
+/// Device forward: returns O and lse (and P when want_p).
+template <typename T>
+void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>& Q,
+                    const DenseMatrix<T>& K, const DenseMatrix<T>& V, const SddmmKind& kind,
+                    std::vector<T>& O, std::vector<T>& lse, std::vector<T>* P) {
+  gf_graph_t dg = device_graph(g, plan);
+  const std::int64_t d = V.cols;
+  const gf_attn_desc desc = make_desc<T>(kind, d);
+  DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), dv = DevBuf::from(V.data);
+  O.assign(static_cast<size_t>(g.num_nodes * d), T(0));
+  lse.assign(static_cast<size_t>(g.num_nodes), T(0));
+  DevBuf dO(sizeof(T) * O.size()), dl(sizeof(T) * lse.size());
+  DevBuf dp(P ? sizeof(T) * static_cast<size_t>(g.num_edges) : 0);
+  GFH_CALL(gf_attn_fwd(dg, &desc, dq.p, dk.p, dv.p, dO.p, dl.p, P ? dp.p : nullptr, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  dO.to(O);
+  dl.to(lse);
+  if (P) {
+    P->assign(static_cast<size_t>(g.num_edges), T(0));
+    dp.to(*P);
+  }
+}
+
+template <typename T>
+ForwardResult<T> run_mode(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                          const DenseMatrix<T>& V, const SddmmKind& kind, const FusionPlan& plan,
+                          Strategy mode) {
+  validate_inputs(g, Q, K, V, kind);
+  const std::int64_t d = V.cols;
+  if (mode == Strategy::Smmf) check_smmf_feasible<T>(g, plan, d);
+  const auto t0 = std::chrono::steady_clock::now();
+  ForwardResult<T> res;
+  res.ctx.g = &g;
+  res.ctx.Q = Q;
+  res.ctx.K = K;
+  res.ctx.V = V;
+  res.ctx.kind = kind;
+  res.ctx.plan = plan.with_strategy(mode);
+  device_forward(g, plan, Q, K, V, kind, res.ctx.O, res.ctx.lse, &res.ctx.P.values);
+  res.O = DenseMatrix<T>(g.num_nodes, d);
+  res.O.data = res.ctx.O;
+  res.counters = model_counters<T>(g, kind, plan, d, mode);
+  res.counters.elapsed_ns = static_cast<std::uint64_t>(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+          .count());
+  return res;
+}
+
+template ForwardResult<float> run_mode<float>(const Graph&, const DenseMatrix<float>&,
+                                              const DenseMatrix<float>&, const DenseMatrix<float>&,
+                                              const SddmmKind&, const FusionPlan&, Strategy);
+template ForwardResult<double> run_mode<double>(const Graph&, const DenseMatrix<double>&,
+                                                const DenseMatrix<double>&,
+                                                const DenseMatrix<double>&, const SddmmKind&,
+                                                const FusionPlan&, Strategy);
+
+ExecCounters backward_counters(const Graph& g, std::int64_t d, std::uint64_t b,
+                               std::uint64_t launches) {
+  ExecCounters c;
+  const std::uint64_t E = static_cast<std::uint64_t>(g.num_edges);
+  const std::uint64_t N = static_cast<std::uint64_t>(g.num_nodes);
+  const std::uint64_t dd = static_cast<std::uint64_t>(d);
+  c.kernel_launches = launches;
+  c.global_bytes_read = 4 * E * dd * b + 2 * E * b;
+  c.global_bytes_written = 2 * N * dd * b + 2 * E * b;
+  if (launches >= 5) {  // edge gradients round-trip in the unfused schedule
+    c.global_bytes_read += 2 * E * b;
+    c.global_bytes_written += 2 * E * b;
+  }
+  return c;
+}
+
+template <typename T>
+GradBundle<T> device_backward(const Graph& g, const ForwardContext<T>& ctx,
+                              const DenseMatrix<T>& dO) {
+  const auto& V = ctx.V;
+  if (dO.rows != g.num_nodes || dO.cols != V.cols)
+    throw KernelError("spmm_backward: dO shape mismatch");
+  validate_inputs(g, ctx.Q, ctx.K, V, ctx.kind);
+  const std::int64_t d = V.cols;
+  const FusionPlan& plan = ctx.plan;
+  std::vector<T> O = ctx.O, lse = ctx.lse;
+  if (O.size() != static_cast<size_t>(g.num_nodes * d) ||
+      lse.size() != static_cast<size_t>(g.num_nodes))
+    device_forward(g, plan, ctx.Q, ctx.K, V, ctx.kind, O, lse, static_cast<std::vector<T>*>(nullptr));  // hand-built ctx
+  gf_graph_t dg = device_graph(g, plan);
+  const gf_attn_desc desc = make_desc<T>(ctx.kind, d);
+  DevBuf dq = DevBuf::from(ctx.Q.data), dk = DevBuf::from(ctx.K.data),
+         dv = DevBuf::from(V.data), dob = DevBuf::from(O), dl = DevBuf::from(lse),
+         ddo = DevBuf::from(dO.data);
+  GradBundle<T> gb;
+  gb.dQ = DenseMatrix<T>(ctx.Q.rows, ctx.Q.cols);
+  gb.dK = DenseMatrix<T>(ctx.K.rows, ctx.K.cols);
+  gb.dV = DenseMatrix<T>(V.rows, V.cols);
+  DevBuf gq(sizeof(T) * gb.dQ.data.size()), gk(sizeof(T) * gb.dK.data.size()),
+      gv(sizeof(T) * gb.dV.data.size());
+  GFH_CALL(gf_attn_bwd(dg, &desc, dq.p, dk.p, dv.p, dob.p, dl.p, ddo.p, gq.p, gk.p, gv.p, nullptr,
+                       nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  gq.to(gb.dQ.data);
+  gk.to(gb.dK.data);
+  gv.to(gb.dV.data);
+  return gb;
+}
+
+}  // namespace detail
+
+template <typename T>
+BackwardResult<T> unfused_backward(const Graph& g, const ForwardContext<T>& ctx,
+                                   const DenseMatrix<T>& dO) {
+  BackwardResult<T> r;
+  r.grads = detail::device_backward(g, ctx, dO);
+  r.counters = detail::backward_counters(g, ctx.V.cols, sizeof(T), 5);
+  return r;
+}
+
+template <typename T>
+BackwardResult<T> fused_backward(const Graph& g, const ForwardContext<T>& ctx,
+                                 const DenseMatrix<T>& dO, const FusionPlan& plan) {
+  bool feasible = true;
+  if (plan.strategy == Strategy::Smmf) {
+    try {
+      detail::check_smmf_feasible<T>(g, plan, ctx.V.cols);
+    } catch (const EngineError&) {
+      feasible = false;
+    }
+  }
+  BackwardResult<T> r;
+  r.grads = detail::device_backward(g, ctx, dO);
+  r.counters = detail::backward_counters(g, ctx.V.cols, sizeof(T), feasible ? 3 : 5);
+  r.counters.fallback_unfused = !feasible;
+  return r;
+}
+
+template <typename T>
+DenseMatrix<T> reference_forward(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                                 const DenseMatrix<T>& V, const SddmmKind& kind) {
+  detail::validate_inputs(g, Q, K, V, kind);
+  std::vector<T> O, lse;
+  detail::device_forward(g, FusionPlan{}, Q, K, V, kind, O, lse,
+                         static_cast<std::vector<T>*>(nullptr));
+  DenseMatrix<T> out(g.num_nodes, V.cols);
+  out.data = std::move(O);
+  return out;
+}
+
+template <typename T>
+T finite_difference_check(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                          const DenseMatrix<T>& V, const SddmmKind& kind, T h) {
+  static_assert(sizeof(T) == 8, "finite differences require f64 inputs");
+  DenseMatrix<T> Qm = Q, Km = K, Vm = V;
+  auto loss = [&] {
+    const auto O = reference_forward(g, Qm, Km, Vm, kind);
+    T s = 0;
+    for (T x : O.data) s += x;
+    if (!std::isfinite(s)) throw KernelError("finite_difference_check: non-finite loss");
+    return s;
+  };
+  ForwardContext<T> ctx;
+  ctx.g = &g;
+  ctx.Q = Q;
+  ctx.K = K;
+  ctx.V = V;
+  ctx.kind = kind;
+  const auto gb = detail::device_backward(g, ctx, DenseMatrix<T>(g.num_nodes, V.cols, T(1)));
+  T worst = 0;
+  auto probe = [&](DenseMatrix<T>& p, const DenseMatrix<T>& grad) {
+    for (size_t i = 0; i < p.data.size(); ++i) {
+      const T keep = p.data[i];
+      p.data[i] = keep + h;
+      const T up = loss();
+      p.data[i] = keep - h;
+      const T dn = loss();
+      p.data[i] = keep;
+      const T fd = (up - dn) / (2 * h);
+      const T a = grad.data[i];
+      worst = std::max(worst, std::abs(a - fd) / std::max({std::abs(a), std::abs(fd), T(1)}));
+    }
+  };
+  probe(Qm, gb.dQ);
+  probe(Km, gb.dK);
+  probe(Vm, gb.dV);
+  return worst;
+}
+
+// ----------------------------------------------------------------- models --
+template <typename T>
+DenseMatrix<T> matmul(const DenseMatrix<T>& A, const DenseMatrix<T>& B) {
+  if (A.cols != B.rows) throw KernelError("matmul: inner dimension mismatch");
+  detail::need_device();
+  DenseMatrix<T> C(A.rows, B.cols);
+  detail::DevBuf a = detail::DevBuf::from(A.data), b = detail::DevBuf::from(B.data);
+  detail::DevBuf c(sizeof(T) * C.data.size());
+  GFH_CALL(gf_gemm(detail::dtype_code<T>(), 0, A.rows, B.cols, A.cols, a.p, b.p, c.p, 0, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  c.to(C.data);
+  return C;
+}
+
+template <typename T>
+DenseMatrix<T> matmul_at_b(const DenseMatrix<T>& A, const DenseMatrix<T>& B) {
+  if (A.rows != B.rows) throw KernelError("matmul_at_b: row count mismatch");
+  detail::need_device();
+  DenseMatrix<T> C(A.cols, B.cols);
+  detail::DevBuf a = detail::DevBuf::from(A.data), b = detail::DevBuf::from(B.data);
+  detail::DevBuf c(sizeof(T) * C.data.size());
+  GFH_CALL(gf_gemm(detail::dtype_code<T>(), 1, A.cols, B.cols, A.rows, a.p, b.p, c.p, 0, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  c.to(C.data);
+  return C;
+}
+
+template <typename T>
+std::pair<DenseMatrix<T>, ConvContext<T>> conv_forward(const ConvSpec& spec, const Graph& g,
+                                                       const DenseMatrix<T>& X,
+                                                       const ConvWeights<T>& w, FusionPlan plan) {
+  const SddmmKind kind = kind_for(spec);
+  plan.dtype_bytes = sizeof(T);
+  plan.strategy = spec.strategy_override ? *spec.strategy_override
+                                         : select_strategy(degree_stats(g), kind,
+                                                           plan.shared_mem_budget_bytes,
+                                                           sizeof(T));
+  ConvContext<T> ctx;
+  ctx.X = X;
+  ForwardResult<T> res;
+  if (spec.model == Model::GAT) {
+    ctx.H = matmul(X, w.W_v);
+    res = run_strategy(g, matmul(ctx.H, w.a_l), matmul(ctx.H, w.a_r), ctx.H, kind, plan);
+  } else {
+    res = run_strategy(g, matmul(X, w.W_q), matmul(X, w.W_k), matmul(X, w.W_v), kind, plan);
+  }
+  ctx.fwd = std::move(res.ctx);
+  ctx.counters = std::move(res.counters);
+  return {std::move(res.O), std::move(ctx)};
+}
+
+template <typename T>
+ConvGrads<T> conv_backward(const ConvSpec& spec, const Graph& g, const ConvContext<T>& ctx,
+                           const ConvWeights<T>& w, const DenseMatrix<T>& dO) {
+  ConvGrads<T> out;
+  out.pipeline = fused_backward(g, ctx.fwd, dO, ctx.fwd.plan).grads;
+  const GradBundle<T>& gb = out.pipeline;
+  if (spec.model == Model::GAT) {
+    // dH = dV + del a_l^T + der a_r^T; da_l = H^T del; da_r = H^T der (models.hpp:143-150)
+    detail::need_device();
+    const std::int64_t n = g.num_nodes, dim = spec.dim;
+    detail::DevBuf hf = detail::DevBuf::from(ctx.H.data), al = detail::DevBuf::from(w.a_l.data),
+                   ar = detail::DevBuf::from(w.a_r.data), dv = detail::DevBuf::from(gb.dV.data),
+                   dl = detail::DevBuf::from(gb.dQ.data), dr = detail::DevBuf::from(gb.dK.data);
+    detail::DevBuf dh(sizeof(T) * n * dim), dal(sizeof(T) * dim), dar(sizeof(T) * dim);
+    GFH_CALL(gf_gat_fanin(detail::dtype_code<T>(), n, 1, static_cast<std::int32_t>(dim), hf.p,
+                          al.p, ar.p, dv.p, dl.p, dr.p, dh.p, dal.p, dar.p, nullptr));
+    DenseMatrix<T> dW(ctx.X.cols, dim);
+    detail::DevBuf x = detail::DevBuf::from(ctx.X.data), dw(sizeof(T) * dW.data.size());
+    GFH_CALL(gf_gemm(detail::dtype_code<T>(), 1, ctx.X.cols, dim, n, x.p, dh.p, dw.p, 0, nullptr));
+    GFH_CALL(gf_stream_sync(nullptr));
+    out.da_l = DenseMatrix<T>(dim, 1);
+    out.da_r = DenseMatrix<T>(dim, 1);
+    dal.to(out.da_l.data);
+    dar.to(out.da_r.data);
+    dw.to(dW.data);
+    out.dW_v = std::move(dW);
+  } else {
+    out.dW_q = matmul_at_b(ctx.X, gb.dQ);
+    out.dW_k = matmul_at_b(ctx.X, gb.dK);
+    out.dW_v = matmul_at_b(ctx.X, gb.dV);
+  }
+  return out;
+}
+
+template <typename T>
+PipelineInputs<T> make_pipeline_inputs(const Graph& g, const ConvSpec& spec, std::uint64_t seed) {
+  PipelineInputs<T> in;
+  in.kind = kind_for(spec);
+  in.V = random_matrix<T>(g.num_nodes, spec.dim, seed + 2);
+  if (spec.model != Model::GAT) {
+    in.Q = random_matrix<T>(g.num_nodes, spec.dim, seed);
+    in.K = random_matrix<T>(g.num_nodes, spec.dim, seed + 1);
+    return in;
+  }
+  // GAT: re-seed el/er until every edge pre-activation is > 1e-3 away from
+  // the LeakyReLU kink (fixture rule of models.hpp:166-190).
+  for (std::uint64_t bump = 0; bump < 64; ++bump) {
+    in.Q = random_matrix<T>(g.num_nodes, 1, seed + bump * 1000);
+    in.K = random_matrix<T>(g.num_nodes, 1, seed + 1 + bump * 1000);
+    T closest = std::numeric_limits<T>::max();
+    for (EdgeId k = 0; k < g.num_edges; ++k)
+      closest = std::min(closest, std::abs(in.Q.data[g.coo_src[k]] + in.K.data[g.coo_dst[k]]));
+    if (g.num_edges == 0 || closest > static_cast<T>(1e-3)) break;
+  }
+  return in;
+}
+
+#define GF_INSTANTIATE(T)                                                                        \
+  template BackwardResult<T> unfused_backward<T>(const Graph&, const ForwardContext<T>&,         \
+                                                 const DenseMatrix<T>&);                         \
+  template BackwardResult<T> fused_backward<T>(const Graph&, const ForwardContext<T>&,           \
+                                               const DenseMatrix<T>&, const FusionPlan&);        \
+  template DenseMatrix<T> reference_forward<T>(const Graph&, const DenseMatrix<T>&,              \
+                                               const DenseMatrix<T>&, const DenseMatrix<T>&,     \
+                                               const SddmmKind&);                                \
+  template DenseMatrix<T> matmul<T>(const DenseMatrix<T>&, const DenseMatrix<T>&);               \
+  template DenseMatrix<T> matmul_at_b<T>(const DenseMatrix<T>&, const DenseMatrix<T>&);          \
+  template std::pair<DenseMatrix<T>, ConvContext<T>> conv_forward<T>(                            \
+      const ConvSpec&, const Graph&, const DenseMatrix<T>&, const ConvWeights<T>&, FusionPlan);  \
+  template ConvGrads<T> conv_backward<T>(const ConvSpec&, const Graph&, const ConvContext<T>&,   \
+                                         const ConvWeights<T>&, const DenseMatrix<T>&);          \
+  template PipelineInputs<T> make_pipeline_inputs<T>(const Graph&, const ConvSpec&, std::uint64_t);
+
+GF_INSTANTIATE(float)
+GF_INSTANTIATE(double)
+template double finite_difference_check<double>(const Graph&, const DenseMatrix<double>&,
+                                                const DenseMatrix<double>&,
+                                                const DenseMatrix<double>&, const SddmmKind&,
+                                                double);
+
+}  // namespace graphfuse

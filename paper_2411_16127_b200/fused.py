@@ -1,0 +1,209 @@
+"""Device-resident, multi-head entry points over the C-ABI (torch tensors in HBM).
+
+PyTorch is plumbing here (device memory, streams); every computation is a
+call into libgraphfuse_cuda.so.  Layout (see include/gf_cuda.h):
+  dot (GT / AGNN): Q, K, V, O are N x (H*D); add (GAT): el, er are N x H.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import AttnDesc, GraphInfo, check, lib
+
+DTYPES = {torch.float32: _capi.GF_F32, torch.float64: _capi.GF_F64}
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class AttnSpec:
+    """SddmmKind (dense.hpp:48-62) + multi-head shape."""
+
+    variant: str = "dot"  # "dot" (GT/AGNN) | "add" (GAT)
+    heads: int = 1
+    head_dim: int = 8
+    scale: float = 1.0
+    slope: float = 0.2
+    l2: bool = False
+
+    def desc(self, dtype) -> AttnDesc:
+        return AttnDesc(DTYPES[dtype], _capi.GF_ADD if self.variant == "add" else _capi.GF_DOT,
+                        int(self.l2), self.heads, self.head_dim, 0, float(self.scale),
+                        float(self.slope))
+
+    @property
+    def F(self) -> int:
+        return self.heads * self.head_dim
+
+    @property
+    def qk_width(self) -> int:
+        return self.heads if self.variant == "add" else self.F
+
+
+class DeviceGraph:
+    """A gf_graph_t: int32 CSR + CSC + degree-bucket schedules in HBM."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        info = GraphInfo()
+        check(lib().gf_graph_get_info(self._h, C.byref(info)), "gf_graph_get_info")
+        self.info = info
+        self.n = int(info.num_nodes)
+        self.e = int(info.num_edges)
+
+    @classmethod
+    def from_host_csr(cls, n, row_ptr, col, csc_ptr, csc_row, cta_threshold=0, stream=None):
+        arrs = [np.ascontiguousarray(a, dtype=np.int64) for a in (row_ptr, col, csc_ptr, csc_row)]
+        h = C.c_void_p()
+        check(lib().gf_graph_create(int(n), int(arrs[1].shape[0]),
+                                    *[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                    int(cta_threshold), _stream(stream), C.byref(h)),
+              "gf_graph_create")
+        return cls(h)
+
+    @classmethod
+    def from_device_csr(cls, n, row_ptr, col, csc_ptr, csc_row, cta_threshold=0, stream=None):
+        ts = [t.to(torch.int32).contiguous() for t in (row_ptr, col, csc_ptr, csc_row)]
+        h = C.c_void_p()
+        check(lib().gf_graph_create_device(int(n), int(ts[1].numel()), *[_p(t) for t in ts],
+                                           int(cta_threshold), _stream(stream), C.byref(h)),
+              "gf_graph_create_device")
+        return cls(h)
+
+    def schedule(self):
+        """(row_order, col_order) as int32 numpy arrays (degree-descending)."""
+        ro = np.zeros(max(self.n, 1), np.int32)
+        co = np.zeros(max(self.n, 1), np.int32)
+        check(lib().gf_graph_get_schedule(self._h, ro.ctypes.data_as(C.c_void_p),
+                                          co.ctypes.data_as(C.c_void_p)), "gf_graph_get_schedule")
+        return ro[: self.n], co[: self.n]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().gf_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_coo_device(n: int, src: torch.Tensor, dst: torch.Tensor, stream=None):
+    """Device from_coo (graph.cpp:61-78): returns int64 (row_ptr, col, csc_ptr,
+    csc_row, csc_perm) on src's device.  Raises GFError on bad ids / duplicates."""
+    src = src.to(torch.int64).contiguous()
+    dst = dst.to(torch.int64).contiguous()
+    e = src.numel()
+    dev = src.device
+    rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    cp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(e, 1), dtype=torch.int64, device=dev)
+    cr = torch.empty(max(e, 1), dtype=torch.int64, device=dev)
+    pm = torch.empty(max(e, 1), dtype=torch.int64, device=dev)
+    bad = C.c_int64(-1)
+    check(lib().gf_from_coo_device(n, e, _p(src), _p(dst), _p(rp), _p(col), _p(cp), _p(cr),
+                                   _p(pm), C.byref(bad), _stream(stream)), "gf_from_coo_device")
+    return rp, col[:e], cp, cr[:e], pm[:e]
+
+
+def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, lse=None,
+                 stream=None):
+    """One fused launch; returns (O, lse) or (O, lse, P)."""
+    n = g.n
+    dt = V.dtype
+    if O is None:
+        O = torch.empty(n, spec.F, dtype=dt, device=V.device)
+    if lse is None:
+        lse = torch.empty(n, spec.heads, dtype=dt, device=V.device)
+    P = torch.empty(max(g.e, 1), spec.heads, dtype=dt, device=V.device) if want_p else None
+    d = spec.desc(dt)
+    check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(lse), _p(P),
+                            _stream(stream)), "gf_attn_fwd")
+    return (O, lse, P[: g.e]) if want_p else (O, lse)
+
+
+def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, lse, dO, dQ=None, dK=None,
+                  dV=None, delta=None, stream=None):
+    """Pass A (CSR) + pass B (CSC); returns (dQ|del, dK|der, dV)."""
+    dt = V.dtype
+    dev = V.device
+    if dQ is None:
+        dQ = torch.empty(g.n, spec.qk_width, dtype=dt, device=dev)
+    if dK is None:
+        dK = torch.empty(g.n, spec.qk_width, dtype=dt, device=dev)
+    if dV is None:
+        dV = torch.empty(g.n, spec.F, dtype=dt, device=dev)
+    d = spec.desc(dt)
+    check(lib().gf_attn_bwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(lse), _p(dO),
+                            _p(dQ), _p(dK), _p(dV), _p(delta), _stream(stream)), "gf_attn_bwd")
+    return dQ, dK, dV
+
+
+class FusedAttention(torch.autograd.Function):
+    """torch.autograd wrapper: forward saves only (O, lse); backward recomputes."""
+
+    @staticmethod
+    def forward(ctx, g, spec, Q, K, V):
+        Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+        O, lse = attn_forward(g, spec, Q, K, V)
+        ctx.g, ctx.spec = g, spec
+        ctx.save_for_backward(Q, K, V, O, lse)
+        return O
+
+    @staticmethod
+    def backward(ctx, dO):
+        Q, K, V, O, lse = ctx.saved_tensors
+        dQ, dK, dV = attn_backward(ctx.g, ctx.spec, Q, K, V, O, lse, dO.contiguous())
+        return None, None, dQ, dK, dV
+
+
+def gemm(A, B, trans_a=False, out=None, accumulate=False, stream=None):
+    """C = A @ B or A^T @ B (gf_gemm, row-major)."""
+    if trans_a:
+        K, M = A.shape
+    else:
+        M, K = A.shape
+    N = B.shape[1]
+    if out is None:
+        out = torch.empty(M, N, dtype=A.dtype, device=A.device)
+    check(lib().gf_gemm(DTYPES[A.dtype], int(trans_a), M, N, K, _p(A), _p(B), _p(out),
+                        int(accumulate), _stream(stream)), "gf_gemm")
+    return out
+
+
+def gat_logits(Hf, a_l, a_r, heads, head_dim, stream=None):
+    n = Hf.shape[0]
+    el = torch.empty(n, heads, dtype=Hf.dtype, device=Hf.device)
+    er = torch.empty_like(el)
+    check(lib().gf_gat_logits(DTYPES[Hf.dtype], n, heads, head_dim, _p(Hf), _p(a_l), _p(a_r),
+                              _p(el), _p(er), _stream(stream)), "gf_gat_logits")
+    return el, er
+
+
+def gat_fanin(Hf, a_l, a_r, dV, d_el, d_er, heads, head_dim, stream=None):
+    n = Hf.shape[0]
+    dH = torch.empty_like(dV)
+    dal = torch.empty(heads * head_dim, dtype=Hf.dtype, device=Hf.device)
+    dar = torch.empty_like(dal)
+    check(lib().gf_gat_fanin(DTYPES[Hf.dtype], n, heads, head_dim, _p(Hf), _p(a_l), _p(a_r),
+                             _p(dV), _p(d_el), _p(d_er), _p(dH), _p(dal), _p(dar),
+                             _stream(stream)), "gf_gat_fanin")
+    return dH, dal, dar
