@@ -20,7 +20,9 @@
  *   - per-destination softmax; empty rows give zero output (kernels.hpp:65-102).
  * Multi-head layout (the reference is single-head and is applied per head):
  *   dot: Q, K, dQ, dK are N x (H*D); add: el, er, del, der are N x H;
- *   V, O, dO, dV are N x (H*D); lse (log-sum-exp of the scores) is N x H;
+ *   V, O, dO, dV are N x (H*D); stats (softmax statistics) is N x H x 2 =
+ *   (row max m, log l) per head with l = sum exp(s - m), so that
+ *   p = exp((s - m) - log l) is recomputed with full relative precision;
  *   all row-major, element type selected by `dtype`.
  *
  * Errors: every function returns GF_OK (0) or a GF_ERR_* code; the message is
@@ -116,20 +118,29 @@ int gf_graph_get_info(gf_graph_t g, gf_graph_info* info);
 int gf_graph_get_schedule(gf_graph_t g, int32_t* row_order, int32_t* col_order);
 
 /* ---- fused forward (replaces run_block_rows, engine.hpp:192-231) ----
- * One launch: SDDMM -> per-destination softmax -> SpMM; writes O and lse
- * only (no E x H tensor).  P (E x H, CSR order) is materialised by a second
+ * One launch: SDDMM -> per-destination softmax -> SpMM; writes O and stats
+ * (N x H x 2) only (no E x H tensor).  P (E x H, CSR order) is materialised by a second
  * recompute launch only when P != NULL (reference ForwardContext::P). */
 int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                const void* V, void* O, void* lse, void* P, void* stream);
+                const void* V, void* O, void* stats, void* P, void* stream);
 
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
  * Pass A over CSR rows (dK or der, and delta = rowsum(dO*O)), pass B over CSC
- * columns (dQ or del, dV).  Attention is recomputed from lse; no E x H
+ * columns (dQ or del, dV).  Attention is recomputed from stats; no E x H
  * tensor is read or written.  `delta` is caller scratch of N x H elements
  * (may be NULL: then the graph's internal scratch is used). */
 int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                const void* V, const void* O, const void* lse, const void* dO, void* dQ,
+                const void* V, const void* O, const void* stats, const void* dO, void* dQ,
                 void* dK, void* dV, void* delta, void* stream);
+/* The two passes separately (same arguments; pass B reads the delta pass A
+ * wrote).  Lets a caller time them apart or overlap pass B's inputs (e.g. an
+ * all-gather of dO/delta in the row-sharded multi-GPU path). */
+int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                     const void* V, const void* O, const void* stats, const void* dO, void* dK,
+                     void* delta, void* stream);
+int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                     const void* V, const void* stats, const void* dO, const void* delta,
+                     void* dQ, void* dV, void* stream);
 
 /* ---- dense projections (replaces matmul / matmul_at_b, models.hpp:58-86) ----
  * C[M x N] = A[M x K] * B[K x N]          (trans_a = 0)

@@ -231,7 +231,8 @@ struct ForwardContext {
   SddmmKind kind;
   FusionPlan plan;
   /// B200: forward statistics for the recompute backward (O and the
-  /// per-row log-sum-exp).  Empty when the context is built by hand; the
+  /// per-row softmax statistics (max, log-sum), 2 per row).  Empty when the
+  /// context is built by hand; the
   /// backward then recomputes them on the device.
   std::vector<T> O, lse;
 };

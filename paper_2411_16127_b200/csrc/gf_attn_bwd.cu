@@ -4,17 +4,17 @@
 // (102-154), and the AGNN chain l2_normalize_backward (76-95).
 //
 // No E x H tensor is stored or read: attention is recomputed per edge from
-// the forward statistics lse (N x H), and the softmax-Jacobian row term
+// the forward statistics (row max, log-sum; N x H x 2), and the softmax-Jacobian row term
 // sum_row P*dP is the per-destination scalar delta = <dO[v], O[v]> (exact
 // identity, since O[v] = sum P V).  Two owner-computes passes, no atomics:
 //
 //   pass A (CSR rows, destination-owned), per in-edge u -> v:
-//       s = score(u, v); p = exp(s - lse[v]); dP = <dO[v], V[u]>;
+//       s = score(u, v); p = exp((s - m[v]) - logl[v]); dP = <dO[v], V[u]>;
 //       dS = p (dP - delta[v])
 //       dot: dK[v] += scale dS Qhat[u]       add: der[v] += dS lrelu'(pre)
 //     also writes delta[v] for pass B.
 //   pass B (CSC columns, source-owned), per out-edge u -> v:
-//       same p, dS from (lse[v], delta[v], K[v] | er[v], dO[v])
+//       same p, dS from (m[v], logl[v], delta[v], K[v] | er[v], dO[v])
 //       dV[u] += p dO[v];  dot: dQ[u] += scale dS Khat[v]
 //                          add: del[u] += dS lrelu'(pre)
 // AGNN's L2 Jacobian is applied in each pass's epilogue on the owned row.
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
   }
   const size_t vrow = static_cast<size_t>(v) * a.F;
 
-  T dov[CPL][CW], delta[CPL], lsev[CPL];
+  T dov[CPL][CW], delta[CPL], mv[CPL], llv[CPL];
   {
     T ov[CPL][CW];
 #pragma unroll
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
 #pragma unroll
       for (int i = 0; i < CW; ++i) s += dov[k][i] * ov[k][i];
       delta[k] = s;
-      lsev[k] = __ldg(a.lse + static_cast<size_t>(v) * a.H + head[k]);
+      ld_stat(a.stats, static_cast<size_t>(v) * a.H + head[k], mv[k], llv[k]);
     }
     head_sum<LPE, CPL>(delta, a.GD);
   }
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
         if (ok[t]) {
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
-            const T p = gexp(s[k] - lsev[k]);
+            const T p = prob(s[k], mv[k], llv[k]);
             const T ds = p * (dp[k] - delta[k]);
             if constexpr (VAR == GF_DOT) {
               const T w = a.scale * ds * rq[k];
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(256) bwd_cols_fast(const BwdArgs<T> a) {
         ok[t] = j < cnt;
         vv[t] = __shfl_sync(kFull, myv, j & 31);
       }
-      T dov[U][CPL][CW], kv[U][CPL][CW], lsev[U][CPL], dlt[U][CPL], erv[U][CPL];
+      T dov[U][CPL][CW], kv[U][CPL][CW], mv[U][CPL], llv[U][CPL], dlt[U][CPL], erv[U][CPL];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
 #pragma unroll
@@ -368,13 +368,14 @@ __global__ void __launch_bounds__(256) bwd_cols_fast(const BwdArgs<T> a) {
               ld_chunk(a.K + vrow + off[k], kv[t][k]);
             else
               erv[t][k] = __ldg(a.K + hi);
-            lsev[t][k] = __ldg(a.lse + hi);
+            ld_stat(a.stats, hi, mv[t][k], llv[t][k]);
             dlt[t][k] = __ldg(a.delta + hi);
           } else {
 #pragma unroll
             for (int i = 0; i < CW; ++i) dov[t][k][i] = T(0), kv[t][k][i] = T(0);
             erv[t][k] = T(0);
-            lsev[t][k] = T(0);
+            mv[t][k] = T(0);
+            llv[t][k] = T(0);
             dlt[t][k] = T(0);
           }
         }
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(256) bwd_cols_fast(const BwdArgs<T> a) {
         if (ok[t]) {
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
-            const T p = gexp(s[k] - lsev[t][k]);
+            const T p = prob(s[k], mv[t][k], llv[t][k]);
             const T ds = p * (dp[k] - dlt[t][k]);
 #pragma unroll
             for (int i = 0; i < CW; ++i) dv[k][i] += p * dov[t][k][i];
@@ -506,18 +507,18 @@ __global__ void __launch_bounds__(128) bwd_rows_generic(const BwdArgs<T> a) {
   __syncwarp();
   T erh, rkh;
   generic_row_setup<T, VAR>(a, v, lane, VAR == GF_DOT ? kvs : nullptr, erh, rkh);
-  T dlt = T(0), lse = T(0), gr = T(0);
+  T dlt = T(0), mh = T(0), llh = T(0), gr = T(0);
   if (lane < a.H) {
     for (int j = 0; j < a.D; ++j) dlt += dos[lane * a.D + j] * __ldg(a.O + vrow + lane * a.D + j);
     a.delta[static_cast<size_t>(v) * a.H + lane] = dlt;
-    lse = __ldg(a.lse + static_cast<size_t>(v) * a.H + lane);
+    ld_stat(a.stats, static_cast<size_t>(v) * a.H + lane, mh, llh);
   }
   for (int i = eb; i < ee; ++i) {
     const int u = __ldg(a.idx + i);
     if (lane < a.H) {
       T rq = T(1), pre = T(0);
       const T s = generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh, &rq, &pre);
-      const T p = gexp(s - lse);
+      const T p = prob(s, mh, llh);
       T dp = T(0);
       for (int j = 0; j < a.D; ++j)
         dp += dos[lane * a.D + j] * __ldg(a.V + static_cast<size_t>(u) * a.F + lane * a.D + j);
@@ -616,7 +617,9 @@ __global__ void __launch_bounds__(128) bwd_cols_generic(const BwdArgs<T> a) {
         pre = elh + __ldg(a.K + hi);
         s = lrelu(pre, a.slope);
       }
-      const T p = gexp(s - __ldg(a.lse + hi));
+      T mh, llh;
+      ld_stat(a.stats, hi, mh, llh);
+      const T p = prob(s, mh, llh);
       T dp = T(0);
       for (int j = 0; j < a.D; ++j) dp += __ldg(a.dO + vrow + lane * a.D + j) * vus[lane * a.D + j];
       const T ds = p * (dp - __ldg(a.delta + hi));
@@ -689,30 +692,40 @@ int set_smem(K kernel, size_t smem) {
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <typename T>
-int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, cudaStream_t s) {
+int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStream_t s) {
   if (g.n == 0) return GF_OK;
   BwdArgs<T> ra = a, ca = a;
   ra.ptr = g.row_ptr, ra.idx = g.col, ra.order = g.row_order, ra.n_cta = g.n_cta_rows;
   ca.ptr = g.csc_ptr, ca.idx = g.csc_row, ca.order = g.col_order, ca.n_cta = g.n_cta_cols;
+  const bool do_a = passes & 1, do_b = passes & 2;
+  const bool dot = variant == GF_DOT;
+  // Each pass picks the fast path independently (both paths write the same
+  // delta), so a misaligned operand of one pass never affects the other.
   const FastShape fs = fast_shape(a.H, a.D, sizeof(T));
-  bool al = aligned16(a.V) && aligned16(a.O) && aligned16(a.dO) && aligned16(a.dV);
-  if (variant == GF_DOT) al = al && aligned16(a.Q) && aligned16(a.K) && aligned16(a.dQ) && aligned16(a.dK);
-  if (fs.ok && al) {
-    ra.GD = ca.GD = fs.gd;
-    const int rb = ra.n_cta + (g.n - ra.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    const int cb = ca.n_cta + (g.n - ca.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const bool fast_a = fs.ok && aligned16(a.V) && aligned16(a.O) && aligned16(a.dO) &&
+                      (!dot || (aligned16(a.Q) && aligned16(a.K) && aligned16(a.dK)));
+  const bool fast_b = fs.ok && aligned16(a.V) && aligned16(a.dO) && aligned16(a.dV) &&
+                      (!dot || (aligned16(a.Q) && aligned16(a.K) && aligned16(a.dQ)));
+  ra.GD = ca.GD = fs.ok ? fs.gd : 1;
+  const int rb = (do_a && fast_a) ? ra.n_cta + (g.n - ra.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+  const int cb = (do_b && fast_b) ? ca.n_cta + (g.n - ca.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+  if (rb || cb) {
+    int rc = GF_OK;
     switch (fs.lpe * 8 + fs.cpl) {
-      case 1 * 8 + 1: return launch_fast_bwd<T, 1, 1>(ra, ca, variant, rb, cb, s);
-      case 2 * 8 + 1: return launch_fast_bwd<T, 2, 1>(ra, ca, variant, rb, cb, s);
-      case 4 * 8 + 1: return launch_fast_bwd<T, 4, 1>(ra, ca, variant, rb, cb, s);
-      case 8 * 8 + 1: return launch_fast_bwd<T, 8, 1>(ra, ca, variant, rb, cb, s);
-      case 16 * 8 + 1: return launch_fast_bwd<T, 16, 1>(ra, ca, variant, rb, cb, s);
-      case 32 * 8 + 1: return launch_fast_bwd<T, 32, 1>(ra, ca, variant, rb, cb, s);
-      case 32 * 8 + 2: return launch_fast_bwd<T, 32, 2>(ra, ca, variant, rb, cb, s);
-      case 32 * 8 + 4: return launch_fast_bwd<T, 32, 4>(ra, ca, variant, rb, cb, s);
-      default: break;
+      case 1 * 8 + 1: rc = launch_fast_bwd<T, 1, 1>(ra, ca, variant, rb, cb, s); break;
+      case 2 * 8 + 1: rc = launch_fast_bwd<T, 2, 1>(ra, ca, variant, rb, cb, s); break;
+      case 4 * 8 + 1: rc = launch_fast_bwd<T, 4, 1>(ra, ca, variant, rb, cb, s); break;
+      case 8 * 8 + 1: rc = launch_fast_bwd<T, 8, 1>(ra, ca, variant, rb, cb, s); break;
+      case 16 * 8 + 1: rc = launch_fast_bwd<T, 16, 1>(ra, ca, variant, rb, cb, s); break;
+      case 32 * 8 + 1: rc = launch_fast_bwd<T, 32, 1>(ra, ca, variant, rb, cb, s); break;
+      case 32 * 8 + 2: rc = launch_fast_bwd<T, 32, 2>(ra, ca, variant, rb, cb, s); break;
+      case 32 * 8 + 4: rc = launch_fast_bwd<T, 32, 4>(ra, ca, variant, rb, cb, s); break;
+      default: set_error("gf_attn_bwd: internal fast-shape dispatch"); return GF_ERR_CUDA;
     }
+    if (rc) return rc;
   }
+  const bool gen_a = do_a && !fast_a, gen_b = do_b && !fast_b;
+  if (!gen_a && !gen_b) return GF_OK;
   if (a.H > 32) {
     set_error("gf_attn_bwd: heads > 32 need a head shape that tiles into 16-byte chunks");
     return GF_ERR_UNSUPPORTED;
@@ -725,25 +738,33 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, cudaStream_t s) {
   }
   const int blocks = (g.n + kGenericWarps - 1) / kGenericWarps;
   int rc;
-  if (variant == GF_DOT) {
-    if ((rc = set_smem(bwd_rows_generic<T, GF_DOT>, sa))) return rc;
-    if ((rc = set_smem(bwd_cols_generic<T, GF_DOT>, sb))) return rc;
-    bwd_rows_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
-    GF_CHECK_LAUNCH("bwd_rows_generic");
-    bwd_cols_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sb, s>>>(ca);
-    GF_CHECK_LAUNCH("bwd_cols_generic");
+  if (dot) {
+    if (gen_a) {
+      if ((rc = set_smem(bwd_rows_generic<T, GF_DOT>, sa))) return rc;
+      bwd_rows_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
+      GF_CHECK_LAUNCH("bwd_rows_generic");
+    }
+    if (gen_b) {
+      if ((rc = set_smem(bwd_cols_generic<T, GF_DOT>, sb))) return rc;
+      bwd_cols_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sb, s>>>(ca);
+      GF_CHECK_LAUNCH("bwd_cols_generic");
+    }
   } else {
-    if ((rc = set_smem(bwd_rows_generic<T, GF_ADD>, sa))) return rc;
-    if ((rc = set_smem(bwd_cols_generic<T, GF_ADD>, sb))) return rc;
-    bwd_rows_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
-    GF_CHECK_LAUNCH("bwd_rows_generic");
-    bwd_cols_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sb, s>>>(ca);
-    GF_CHECK_LAUNCH("bwd_cols_generic");
+    if (gen_a) {
+      if ((rc = set_smem(bwd_rows_generic<T, GF_ADD>, sa))) return rc;
+      bwd_rows_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
+      GF_CHECK_LAUNCH("bwd_rows_generic");
+    }
+    if (gen_b) {
+      if ((rc = set_smem(bwd_cols_generic<T, GF_ADD>, sb))) return rc;
+      bwd_cols_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sb, s>>>(ca);
+      GF_CHECK_LAUNCH("bwd_cols_generic");
+    }
   }
   return GF_OK;
 }
 
-template int launch_bwd<float>(const DevGraph&, BwdArgs<float>, int, cudaStream_t);
-template int launch_bwd<double>(const DevGraph&, BwdArgs<double>, int, cudaStream_t);
+template int launch_bwd<float>(const DevGraph&, BwdArgs<float>, int, int, cudaStream_t);
+template int launch_bwd<double>(const DevGraph&, BwdArgs<double>, int, int, cudaStream_t);
 
 }  // namespace gfb

@@ -16,7 +16,7 @@
 //     with 16-byte loads (128-bit vectorised, coalesced gathers of V[src] and
 //     Q[src] / el[src]), 32/LPE edges per step, unrolled U-deep for MLP.
 // Nothing of size E x H is written; the only outputs are O (N x F) and
-// lse (N x H), the statistics the recompute backward needs.
+// the softmax statistics (N x H x 2: row max, log-sum) the backward needs.
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 
@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
       for (int i = 0; i < CW; ++i) o[i] = acc[k][i] * r;
       st_chunk(a.O + static_cast<size_t>(v) * a.F + off[k], o);
       if ((c + k * LPE) % a.GD == 0)
-        a.lse[static_cast<size_t>(v) * a.H + head[k]] =
-            l[k] == T(0) ? ninf<T>() : m[k] + glog(l[k]);
+        st_stat(a.stats, static_cast<size_t>(v) * a.H + head[k], l[k] == T(0) ? ninf<T>() : m[k],
+                l[k] == T(0) ? T(0) : glog(l[k]));
     }
   }
 }
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   }
   if (lane < a.H) {
     lh[lane] = l;
-    a.lse[static_cast<size_t>(v) * a.H + lane] = l == T(0) ? ninf<T>() : m + glog(l);
+    st_stat(a.stats, static_cast<size_t>(v) * a.H + lane, l == T(0) ? ninf<T>() : m,
+            l == T(0) ? T(0) : glog(l));
   }
   __syncwarp();
   for (int f = lane; f < a.F; f += 32) {
@@ -307,11 +308,12 @@ __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __re
   const int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
   T erh, rkh;
   generic_row_setup<T, VAR>(a, v, lane, nullptr, erh, rkh);
-  const T lse = a.lse[static_cast<size_t>(v) * a.H + lane];
+  T m, ll;
+  ld_stat(a.stats, static_cast<size_t>(v) * a.H + lane, m, ll);
   for (int i = eb; i < ee; ++i) {
     const int u = __ldg(a.idx + i);
     P[static_cast<size_t>(i) * a.H + lane] =
-        gexp(generic_score<T, VAR>(a, u, v, lane, nullptr, erh, rkh) - lse);
+        prob(generic_score<T, VAR>(a, u, v, lane, nullptr, erh, rkh), m, ll);
   }
 }
 

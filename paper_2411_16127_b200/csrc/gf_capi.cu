@@ -93,7 +93,7 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
   a.K = static_cast<const T*>(K);
   a.V = static_cast<const T*>(V);
   a.O = static_cast<T*>(O);
-  a.lse = static_cast<T*>(lse);
+  a.stats = static_cast<T*>(lse);
   return a;
 }
 
@@ -109,7 +109,7 @@ int fwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
 template <typename T>
 int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, const void* V,
              const void* O, const void* lse, const void* dO, void* dQ, void* dK, void* dV,
-             void* delta, cudaStream_t s) {
+             void* delta, int passes, cudaStream_t s) {
   gfb::BwdArgs<T> a{};
   a.n = g->n;
   a.H = d.heads;
@@ -123,7 +123,7 @@ int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
   a.K = static_cast<const T*>(K);
   a.V = static_cast<const T*>(V);
   a.O = static_cast<const T*>(O);
-  a.lse = static_cast<const T*>(lse);
+  a.stats = static_cast<const T*>(lse);
   a.dO = static_cast<const T*>(dO);
   a.dQ = static_cast<T*>(dQ);
   a.dK = static_cast<T*>(dK);
@@ -141,7 +141,7 @@ int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
     }
     a.delta = static_cast<T*>(g->scratch);
   }
-  return gfb::launch_bwd<T>(*g, a, d.variant, s);
+  return gfb::launch_bwd<T>(*g, a, d.variant, passes, s);
 }
 
 }  // namespace
@@ -176,6 +176,35 @@ extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q
   }
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
-             ? bwd_impl<float>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, s)
-             : bwd_impl<double>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, s);
+             ? bwd_impl<float>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, 3, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, 3, s);
+}
+
+extern "C" int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const void* Q,
+                                const void* K, const void* V, const void* O, const void* stats,
+                                const void* dO, void* dK, void* delta, void* stream) {
+  if (int rc = check_desc(desc, "gf_attn_bwd_rows")) return rc;
+  if (!g || (g->n > 0 && (!Q || !K || !V || !O || !stats || !dO || !dK || !delta))) {
+    gfb::set_error("gf_attn_bwd_rows: null graph or operand");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  return desc->dtype == GF_F32
+             ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, delta, 1, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, delta, 1, s);
+}
+
+extern "C" int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q,
+                                const void* K, const void* V, const void* stats, const void* dO,
+                                const void* delta, void* dQ, void* dV, void* stream) {
+  if (int rc = check_desc(desc, "gf_attn_bwd_cols")) return rc;
+  if (!g || (g->n > 0 && (!Q || !K || !V || !stats || !dO || !delta || !dQ || !dV))) {
+    gfb::set_error("gf_attn_bwd_cols: null graph or operand");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  void* dl = const_cast<void*>(delta);
+  return desc->dtype == GF_F32
+             ? bwd_impl<float>(g, *desc, Q, K, V, nullptr, stats, dO, dQ, nullptr, dV, dl, 2, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, nullptr, stats, dO, dQ, nullptr, dV, dl, 2, s);
 }

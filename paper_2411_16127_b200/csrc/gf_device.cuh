@@ -46,6 +46,30 @@ __device__ __forceinline__ T ninf() {
   return -INFINITY;
 }
 
+// Softmax statistics per (row, head): (m, log l) with m the row max and l the
+// sum of exp(s - m).  p = exp((s - m) - log l) keeps full relative precision
+// for any score magnitude (a single fused lse = m + log l would lose
+// ulp(|m|) absolute, i.e. ~6e-5 relative at |s| ~ 1e3 in fp32).
+template <typename T>
+__device__ __forceinline__ void ld_stat(const T* __restrict__ st, size_t i, T& m, T& ll) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(st) + i);
+    m = v.x, ll = v.y;
+  } else {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(st) + i);
+    m = v.x, ll = v.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st_stat(T* st, size_t i, T m, T ll) {
+  st[2 * i] = m;
+  st[2 * i + 1] = ll;
+}
+template <typename T>
+__device__ __forceinline__ T prob(T s, T m, T ll) {
+  return gexp((s - m) - ll);
+}
+
 template <typename T>
 __device__ __forceinline__ T lrelu(T x, T slope) {
   return x >= T(0) ? x : slope * x;  // kernels.hpp:44

@@ -75,7 +75,7 @@ struct FwdArgs {
   const T* K;  // dot: N x F; add: er N x H
   const T* V;
   T* O;
-  T* lse;
+  T* stats;  // N x H x 2: (row max, log sum-exp) per head
 };
 
 template <typename T>
@@ -91,7 +91,7 @@ struct BwdArgs {
   const T* K;
   const T* V;
   const T* O;
-  const T* lse;
+  const T* stats;
   const T* dO;
   T* delta;  // pass A writes, pass B reads
   T* dQ;     // pass B (dot) / del (add)
@@ -105,8 +105,9 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a, int variant, cudaStream_t
 template <typename T>
 int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T* P,
                          cudaStream_t s);
+// passes: bit 0 = pass A (CSR rows), bit 1 = pass B (CSC columns).
 template <typename T>
-int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, cudaStream_t s);
+int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStream_t s);
 
 // Fast-path eligibility: chunk = 16 bytes; D a multiple of the chunk width,
 // chunks per head a power of two, F/CW a power of two <= 128, 16 B alignment.

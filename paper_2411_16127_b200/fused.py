@@ -124,23 +124,30 @@ def from_coo_device(n: int, src: torch.Tensor, dst: torch.Tensor, stream=None):
     return rp, col[:e], cp, cr[:e], pm[:e]
 
 
-def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, lse=None,
+def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, stats=None,
                  stream=None):
-    """One fused launch; returns (O, lse) or (O, lse, P)."""
+    """One fused launch; returns (O, stats) or (O, stats, P).
+
+    stats is N x H x 2: (row max, log sum-exp) per head; lse = m + log l."""
     n = g.n
     dt = V.dtype
     if O is None:
         O = torch.empty(n, spec.F, dtype=dt, device=V.device)
-    if lse is None:
-        lse = torch.empty(n, spec.heads, dtype=dt, device=V.device)
+    if stats is None:
+        stats = torch.empty(n, spec.heads, 2, dtype=dt, device=V.device)
     P = torch.empty(max(g.e, 1), spec.heads, dtype=dt, device=V.device) if want_p else None
     d = spec.desc(dt)
-    check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(lse), _p(P),
+    check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats), _p(P),
                             _stream(stream)), "gf_attn_fwd")
-    return (O, lse, P[: g.e]) if want_p else (O, lse)
+    return (O, stats, P[: g.e]) if want_p else (O, stats)
 
 
-def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, lse, dO, dQ=None, dK=None,
+def lse_of(stats):
+    """log-sum-exp per (row, head) from the (m, log l) statistics."""
+    return stats[..., 0] + stats[..., 1]
+
+
+def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, stats, dO, dQ=None, dK=None,
                   dV=None, delta=None, stream=None):
     """Pass A (CSR) + pass B (CSC); returns (dQ|del, dK|der, dV)."""
     dt = V.dtype
@@ -152,26 +159,40 @@ def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, lse, dO, dQ=None, 
     if dV is None:
         dV = torch.empty(g.n, spec.F, dtype=dt, device=dev)
     d = spec.desc(dt)
-    check(lib().gf_attn_bwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(lse), _p(dO),
+    check(lib().gf_attn_bwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats), _p(dO),
                             _p(dQ), _p(dK), _p(dV), _p(delta), _stream(stream)), "gf_attn_bwd")
     return dQ, dK, dV
 
 
+def attn_backward_rows(g, spec, Q, K, V, O, stats, dO, dK, delta, stream=None):
+    """Pass A only: dK | der and delta (CSR rows)."""
+    d = spec.desc(V.dtype)
+    check(lib().gf_attn_bwd_rows(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats),
+                                 _p(dO), _p(dK), _p(delta), _stream(stream)), "gf_attn_bwd_rows")
+
+
+def attn_backward_cols(g, spec, Q, K, V, stats, dO, delta, dQ, dV, stream=None):
+    """Pass B only: dQ | del and dV (CSC columns), reading pass A's delta."""
+    d = spec.desc(V.dtype)
+    check(lib().gf_attn_bwd_cols(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(stats), _p(dO),
+                                 _p(delta), _p(dQ), _p(dV), _stream(stream)), "gf_attn_bwd_cols")
+
+
 class FusedAttention(torch.autograd.Function):
-    """torch.autograd wrapper: forward saves only (O, lse); backward recomputes."""
+    """torch.autograd wrapper: forward saves only (O, stats); backward recomputes."""
 
     @staticmethod
     def forward(ctx, g, spec, Q, K, V):
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
-        O, lse = attn_forward(g, spec, Q, K, V)
+        O, stats = attn_forward(g, spec, Q, K, V)
         ctx.g, ctx.spec = g, spec
-        ctx.save_for_backward(Q, K, V, O, lse)
+        ctx.save_for_backward(Q, K, V, O, stats)
         return O
 
     @staticmethod
     def backward(ctx, dO):
-        Q, K, V, O, lse = ctx.saved_tensors
-        dQ, dK, dV = attn_backward(ctx.g, ctx.spec, Q, K, V, O, lse, dO.contiguous())
+        Q, K, V, O, stats = ctx.saved_tensors
+        dQ, dK, dV = attn_backward(ctx.g, ctx.spec, Q, K, V, O, stats, dO.contiguous())
         return None, None, dQ, dK, dV
 
 

@@ -72,10 +72,10 @@ def run_device(g, spec, Q, K, V, dO, cta_threshold=0, want_p=False):
     dev = torch.device("cuda:0")
     t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (Q, K, V, dO)]
     out = fused.attn_forward(dg, spec, t[0], t[1], t[2], want_p=want_p)
-    O, lse = out[0], out[1]
-    dQ, dK, dV = fused.attn_backward(dg, spec, t[0], t[1], t[2], O, lse, t[3])
+    O, stats = out[0], out[1]
+    dQ, dK, dV = fused.attn_backward(dg, spec, t[0], t[1], t[2], O, stats, t[3])
     torch.cuda.synchronize()
-    res = {"O": O.cpu().numpy(), "lse": lse.cpu().numpy(), "dQ": dQ.cpu().numpy(),
+    res = {"O": O.cpu().numpy(), "lse": fused.lse_of(stats).cpu().numpy(), "dQ": dQ.cpu().numpy(),
            "dK": dK.cpu().numpy(), "dV": dV.cpu().numpy()}
     if want_p:
         res["P"] = out[2].cpu().numpy()
