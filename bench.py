@@ -117,12 +117,14 @@ def algorithmic_bytes(kernel, layer, n, e, H, D, b=4, idx=4):
     F = H * D
     dot = layer != "gat"
     qk = F if dot else H  # Q|el and K|er width
-    if kernel == "fwd":  # ptr, order, col; V[src] + Q|el[src]; K|er[v]; O, stats
-        return idx * (2 * n + 1 + e) + b * (e * (F + qk) + n * (qk + F + 2 * H))
-    if kernel == "bwd_rows":  # + dO, O, stats, K|er rows; writes dK|der, delta
-        return idx * (2 * n + 1 + e) + b * (e * (F + qk) + n * (2 * F + 2 * H + 2 * qk + H))
-    if kernel == "bwd_cols":  # gathers dO, K|er, stats, delta of dst; own V, Q|el; writes dV, dQ|del
-        return idx * (2 * n + 1 + e) + b * (e * (F + qk + 3 * H) + n * (2 * F + 2 * qk))
+    rec = 4 * H  # softmax record {m, log2 l, aux, delta} per head
+    topo = idx * (2 * n + 1 + e)  # row pointer, schedule, neighbour ids
+    if kernel == "fwd":  # gather V, Q|el of src; own K|er; write O + records
+        return topo + b * (e * (F + qk) + n * (qk + F + rec))
+    if kernel == "bwd_rows":  # gather V, Q|el of src; own dO, O, K (dot), record; write dK|der, delta
+        return topo + b * (e * (F + qk) + n * (2 * F + (F if dot else 0) + rec + qk + H))
+    if kernel == "bwd_cols":  # gather dO, K (dot), record of dst; own V, Q|el; write dV, dQ|del
+        return topo + b * (e * (F + (F if dot else 0) + rec) + n * (2 * F + 2 * qk))
     raise ValueError(kernel)
 
 
@@ -366,9 +368,8 @@ def run_ours(args, rank, world):
     amp = 2.0 if layer == "gat" else 1.0
     Q, K, V, dO = u(n, qk, amp=amp), u(n, qk, amp=amp), u(n, F), u(n, F)
     O = torch.empty(n, F, device=dev)
-    stats = torch.empty(n, H, 2, device=dev)
+    stats = torch.empty(n, H, 4, device=dev)
     dQ, dK, dV = torch.empty(n, qk, device=dev), torch.empty(n, qk, device=dev), torch.empty(n, F, device=dev)
-    delta = torch.empty(n, H, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream()
 
@@ -378,10 +379,10 @@ def run_ours(args, rank, world):
         fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream)
         if ev:
             ev[1].record(stream)
-        fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK, delta, stream=stream)
+        fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK, stream=stream)
         if ev:
             ev[2].record(stream)
-        fused.attn_backward_cols(dg, spec, Q, K, V, stats, dO, delta, dQ, dV, stream=stream)
+        fused.attn_backward_cols(dg, spec, Q, K, V, stats, dO, dQ, dV, stream=stream)
         if ev:
             ev[3].record(stream)
 

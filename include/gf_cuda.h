@@ -20,10 +20,14 @@
  *   - per-destination softmax; empty rows give zero output (kernels.hpp:65-102).
  * Multi-head layout (the reference is single-head and is applied per head):
  *   dot: Q, K, dQ, dK are N x (H*D); add: el, er, del, der are N x H;
- *   V, O, dO, dV are N x (H*D); stats (softmax statistics) is N x H x 2 =
- *   (row max m, log l) per head with l = sum exp(s - m), so that
- *   p = exp((s - m) - log l) is recomputed with full relative precision;
- *   all row-major, element type selected by `dtype`.
+ *   V, O, dO, dV are N x (H*D); all row-major, element type `dtype`.
+ *   stats is N x H x 4 softmax records {m, log2 l, aux, delta} per (row,
+ *   head): m = row max of the scores, l = sum exp(s - m) (so p is recomputed
+ *   as exp((s - m) - log l) with full relative precision for any |s|),
+ *   aux = er (GAT) or 1/max(||K||, eps) (AGNN), delta = <dO, O> (written by
+ *   backward pass A).  Base pointers must be 32-byte aligned for the 256-bit
+ *   gather path (torch / cudaMalloc allocations are); other alignments fall
+ *   back to the generic kernels.
  *
  * Errors: every function returns GF_OK (0) or a GF_ERR_* code; the message is
  * available from gf_last_error() (thread-local).  Launch failures are
@@ -118,29 +122,29 @@ int gf_graph_get_info(gf_graph_t g, gf_graph_info* info);
 int gf_graph_get_schedule(gf_graph_t g, int32_t* row_order, int32_t* col_order);
 
 /* ---- fused forward (replaces run_block_rows, engine.hpp:192-231) ----
- * One launch: SDDMM -> per-destination softmax -> SpMM; writes O and stats
- * (N x H x 2) only (no E x H tensor).  P (E x H, CSR order) is materialised by a second
- * recompute launch only when P != NULL (reference ForwardContext::P). */
+ * One launch: SDDMM -> per-destination softmax -> SpMM; writes O and the
+ * stats records only (no E x H tensor).  P (E x H, CSR order) is
+ * materialised by a second recompute launch only when P != NULL (reference
+ * ForwardContext::P). */
 int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                 const void* V, void* O, void* stats, void* P, void* stream);
 
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
- * Pass A over CSR rows (dK or der, and delta = rowsum(dO*O)), pass B over CSC
- * columns (dQ or del, dV).  Attention is recomputed from stats; no E x H
- * tensor is read or written.  `delta` is caller scratch of N x H elements
- * (may be NULL: then the graph's internal scratch is used). */
+ * Pass A over CSR rows (dK or der, and delta into stats), pass B over CSC
+ * columns (dQ or del, dV).  Attention is recomputed from the stats records;
+ * no E x H tensor is read or written.  stats is read-write (delta). */
 int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                const void* V, const void* O, const void* stats, const void* dO, void* dQ,
-                void* dK, void* dV, void* delta, void* stream);
+                const void* V, const void* O, void* stats, const void* dO, void* dQ, void* dK,
+                void* dV, void* stream);
 /* The two passes separately (same arguments; pass B reads the delta pass A
  * wrote).  Lets a caller time them apart or overlap pass B's inputs (e.g. an
- * all-gather of dO/delta in the row-sharded multi-GPU path). */
+ * all-gather of dO and the records in the row-sharded multi-GPU path). */
 int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                     const void* V, const void* O, const void* stats, const void* dO, void* dK,
-                     void* delta, void* stream);
+                     const void* V, const void* O, void* stats, const void* dO, void* dK,
+                     void* stream);
 int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                     const void* V, const void* stats, const void* dO, const void* delta,
-                     void* dQ, void* dV, void* stream);
+                     const void* V, const void* stats, const void* dO, void* dQ, void* dV,
+                     void* stream);
 
 /* ---- dense projections (replaces matmul / matmul_at_b, models.hpp:58-86) ----
  * C[M x N] = A[M x K] * B[K x N]          (trans_a = 0)

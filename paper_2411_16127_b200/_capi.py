@@ -53,11 +53,11 @@ SIGNATURES = {
     "gf_graph_get_schedule": (C.c_int, [_vp, _vp, _vp]),
     "gf_attn_fwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                              _vp, _vp, _vp]),
+                              _vp, _vp]),
     "gf_attn_bwd_rows": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                   _vp, _vp]),
+                                   _vp]),
     "gf_attn_bwd_cols": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                   _vp, _vp]),
+                                   _vp]),
     "gf_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp,
                           C.c_int32, _vp]),
     "gf_gat_logits": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,

@@ -9,14 +9,15 @@
 //     the longest rows start first (LPT);
 //   * rows with degree >= cta_threshold get a whole 8-warp CTA: the edge range
 //     is split into 8 balanced slices (the reference's warp_balance rule,
-//     schedule.cpp:42-60), each warp runs an online (max,sum) softmax over its
-//     slice in registers, and the 8 partial states are merged in shared
+//     schedule.cpp:42-60), each warp runs an online (max, sum) softmax over
+//     its slice in registers, and the 8 partial states are merged in shared
 //     memory in a fixed order (deterministic);
-//   * every other row is warp-per-row: LPE lanes cover one edge's feature row
-//     with 16-byte loads (128-bit vectorised, coalesced gathers of V[src] and
-//     Q[src] / el[src]), 32/LPE edges per step, unrolled U-deep for MLP.
-// Nothing of size E x H is written; the only outputs are O (N x F) and
-// the softmax statistics (N x H x 2: row max, log-sum) the backward needs.
+//   * every other row is warp-per-row.
+// Lane mapping: a lane owns (a 2-chunk slice of) ONE head and gathers it with
+// 256-bit loads (LDG.E.256, one full 32 B sector per lane), so per-head score
+// / softmax work is done once per edge, not once per 16 B chunk; 32/LPE edges
+// per warp step, unrolled U deep.  Nothing of size E x H is written: outputs
+// are O (N x F) and the per-(row, head) softmax records (gf_device.cuh Rec).
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 
@@ -24,23 +25,24 @@ namespace gfb {
 
 namespace {
 
-template <typename T, int CW>
-__device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[CW], T m2, T l2,
-                                            const T (&acc2)[CW]) {
+template <typename T, int N>
+__device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
+                                            const T (&acc2)[N]) {
   const T mn = m > m2 ? m : m2;
-  if (!(mn > ninf<T>())) return;  // both empty (or NaN max: keep ours)
-  const T ca = gexp(m - mn), cb = gexp(m2 - mn);
+  if (!(mn > ninf<T>())) return;  // both empty
+  const T ca = expd(m - mn), cb = expd(m2 - mn);
   l = l * ca + l2 * cb;
 #pragma unroll
-  for (int i = 0; i < CW; ++i) acc[i] = acc[i] * ca + acc2[i] * cb;
+  for (int i = 0; i < N; ++i) acc[i] = acc[i] * ca + acc2[i] * cb;
   m = mn;
 }
 
-template <typename T, int LPE, int CPL, int VAR>
+template <typename T, int CB, int LPE, int CPL, int VAR>
 __global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
-  constexpr int CW = Chunk<T>::W;
+  constexpr int CW = Chunk<T, CB>::W;
+  constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? 4 : (CPL == 2 ? 2 : 1);
+  constexpr int U = CPL == 1 ? 4 : 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPE, sub = lane / LPE;
   const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
@@ -55,189 +57,150 @@ __global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
   int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
 
-  int off[CPL], head[CPL];
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    const int ch = c + k * LPE;
-    off[k] = ch * CW;
-    head[k] = ch / a.GD;
-  }
+  const int h = c / a.LPH;
+  const int off = h * a.D + (c % a.LPH) * NE;  // first element owned by this lane
+  const T* __restrict__ Vb = a.V + off;
+  const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
+  const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
 
   // Destination-side operands stay in registers for the whole row.
-  T kv[CPL][CW];
-  T erv[CPL];
-  T rk[CPL];
+  T kv[NE];
+  T erv = T(0), rk = T(1);
   if constexpr (VAR == GF_DOT) {
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) ld_chunk(a.K + static_cast<size_t>(v) * a.F + off[k], kv[k]);
+    for (int k = 0; k < CPL; ++k)
+      ld_own<T, CB>(a.K + static_cast<size_t>(v) * a.F + off + k * CW,
+                    *reinterpret_cast<T(*)[CW]>(kv + k * CW));
     if (a.l2) {
+      T s = T(0);
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        T s = T(0);
-#pragma unroll
-        for (int i = 0; i < CW; ++i) s += kv[k][i] * kv[k][i];
-        rk[k] = s;
-      }
-      head_sum<LPE, CPL>(rk, a.GD);
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) rk[k] = inv_norm(rk[k]);
+      for (int i = 0; i < NE; ++i) s += kv[i] * kv[i];
+      rk = inv_norm(head_sum(s, a.LPH));
     }
   } else {
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) erv[k] = __ldg(a.K + static_cast<size_t>(v) * a.H + head[k]);
+    erv = __ldg(a.K + static_cast<size_t>(v) * a.H + h);
   }
 
-  T m[CPL], l[CPL], acc[CPL][CW];
+  T m = ninf<T>(), l = T(0), acc[NE];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    m[k] = ninf<T>();
-    l[k] = T(0);
-#pragma unroll
-    for (int i = 0; i < CW; ++i) acc[k][i] = T(0);
-  }
+  for (int i = 0; i < NE; ++i) acc[i] = T(0);
 
   for (int base = eb; base < ee; base += 32) {
     const int cnt = min(32, ee - base);
     const int myu = lane < cnt ? __ldg(a.idx + base + lane) : 0;
 #pragma unroll 1
     for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
-      int u[U];
       bool ok[U];
+      T vv[U][NE], qv[U][NE], s[U];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         const int j = j0 + t * EPW + sub;
         ok[t] = j < cnt;
-        u[t] = __shfl_sync(kFull, myu, j & 31);
-      }
-      T vv[U][CPL][CW];
-      T qv[U][CPL][CW];
-      T elv[U][CPL];
+        const int u = __shfl_sync(kFull, myu, j & 31);
+        const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
 #pragma unroll
-      for (int t = 0; t < U; ++t) {
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          if (ok[t]) {
-            ld_chunk(a.V + static_cast<size_t>(u[t]) * a.F + off[k], vv[t][k]);
-            if constexpr (VAR == GF_DOT)
-              ld_chunk(a.Q + static_cast<size_t>(u[t]) * a.F + off[k], qv[t][k]);
-            else
-              elv[t][k] = __ldg(a.Q + static_cast<size_t>(u[t]) * a.H + head[k]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < CW; ++i) vv[t][k][i] = T(0), qv[t][k][i] = T(0);
-            elv[t][k] = T(0);
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        T s[CPL];
+        for (int k = 0; k < CPL; ++k)
+          ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
         if constexpr (VAR == GF_DOT) {
-          T q2[CPL];
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            T d = T(0), qq = T(0);
-#pragma unroll
-            for (int i = 0; i < CW; ++i) {
-              d += qv[t][k][i] * kv[k][i];
-              qq += qv[t][k][i] * qv[t][k][i];
-            }
-            s[k] = d;
-            q2[k] = qq;
-          }
-          head_sum<LPE, CPL>(s, a.GD);
-          if (a.l2) {
-            head_sum<LPE, CPL>(q2, a.GD);
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) s[k] = a.scale * s[k] * (inv_norm(q2[k]) * rk[k]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) s[k] = a.scale * s[k];
-          }
+          for (int k = 0; k < CPL; ++k)
+            ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
         } else {
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) s[k] = lrelu(elv[t][k] + erv[k], a.slope);
+          s[t] = __ldg(Qb + uu * qs);
         }
-        if (ok[t]) {
+      }
+      T smax = ninf<T>();
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            if (s[k] > m[k]) {  // lazy rescale: only when the running max moves
-              const T corr = gexp(m[k] - s[k]);
-              l[k] *= corr;
+      for (int t = 0; t < U; ++t) {
+        if constexpr (VAR == GF_DOT) {
+          T d = T(0), qq = T(0);
 #pragma unroll
-              for (int i = 0; i < CW; ++i) acc[k][i] *= corr;
-              m[k] = s[k];
-            }
-            const T p = gexp(s[k] - m[k]);
-            l[k] += p;
-#pragma unroll
-            for (int i = 0; i < CW; ++i) acc[k][i] += p * vv[t][k][i];
+          for (int i = 0; i < NE; ++i) {
+            d += qv[t][i] * kv[i];
+            qq += qv[t][i] * qv[t][i];
           }
+          d = head_sum(d, a.LPH);
+          if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
+          s[t] = a.scale * d;
+        } else {
+          s[t] = lrelu(s[t] + erv, a.slope);
         }
+        s[t] = ok[t] ? s[t] : ninf<T>();
+        smax = s[t] > smax ? s[t] : smax;
+      }
+      // Lazy rescale, warp-uniform: only when some lane's running max moves.
+      if (__any_sync(kFull, smax > m)) {
+        const T mn = smax > m ? smax : m;
+        const T corr = m == mn ? T(1) : expd(m - mn);
+        l *= corr;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) acc[i] *= corr;
+        m = mn;
+      }
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const T p = ok[t] ? expd(s[t] - m) : T(0);
+        l += p;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
       }
     }
   }
 
-  // Merge the EPW edge slots of the warp (butterfly: every lane ends with the
-  // warp's state).
+  // Merge the EPW edge slots of the warp (butterfly: every lane ends with
+  // the warp's state).
 #pragma unroll
   for (int o = LPE; o < 32; o <<= 1) {
+    T acc2[NE];
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      T acc2[CW];
-#pragma unroll
-      for (int i = 0; i < CW; ++i) acc2[i] = __shfl_xor_sync(kFull, acc[k][i], o);
-      const T m2 = __shfl_xor_sync(kFull, m[k], o);
-      const T l2 = __shfl_xor_sync(kFull, l[k], o);
-      merge_state<T, CW>(m[k], l[k], acc[k], m2, l2, acc2);
-    }
+    for (int i = 0; i < NE; ++i) acc2[i] = __shfl_xor_sync(kFull, acc[i], o);
+    const T m2 = __shfl_xor_sync(kFull, m, o);
+    const T l2 = __shfl_xor_sync(kFull, l, o);
+    merge_state<T, NE>(m, l, acc, m2, l2, acc2);
   }
 
   if (cta) {
     // Shared-memory merge of the 8 warp slices, fixed order w = 0..7.
-    __shared__ T sm[kWarpsPerBlock][LPE * CPL][2 + CW];
+    __shared__ T sm[kWarpsPerBlock][LPE][2 + NE];
     if (sub == 0) {
+      T* d = sm[warp][c];
+      d[0] = m;
+      d[1] = l;
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        T* d = sm[warp][c * CPL + k];
-        d[0] = m[k];
-        d[1] = l[k];
-#pragma unroll
-        for (int i = 0; i < CW; ++i) d[2 + i] = acc[k][i];
-      }
+      for (int i = 0; i < NE; ++i) d[2 + i] = acc[i];
     }
     __syncthreads();
     if (warp != 0) return;
     if (sub == 0) {
+      const T* d0 = sm[0][c];
+      m = d0[0];
+      l = d0[1];
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        const T* d0 = sm[0][c * CPL + k];
-        m[k] = d0[0];
-        l[k] = d0[1];
+      for (int i = 0; i < NE; ++i) acc[i] = d0[2 + i];
+      for (int w = 1; w < kWarpsPerBlock; ++w) {
+        const T* d = sm[w][c];
+        T acc2[NE];
 #pragma unroll
-        for (int i = 0; i < CW; ++i) acc[k][i] = d0[2 + i];
-        for (int w = 1; w < kWarpsPerBlock; ++w) {
-          const T* d = sm[w][c * CPL + k];
-          T acc2[CW];
-#pragma unroll
-          for (int i = 0; i < CW; ++i) acc2[i] = d[2 + i];
-          merge_state<T, CW>(m[k], l[k], acc[k], d[0], d[1], acc2);
-        }
+        for (int i = 0; i < NE; ++i) acc2[i] = d[2 + i];
+        merge_state<T, NE>(m, l, acc, d[0], d[1], acc2);
       }
     }
   }
 
   if (sub == 0) {
+    const T r = l == T(0) ? T(0) : T(1) / l;
+    T o[NE];
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const T r = l[k] == T(0) ? T(0) : T(1) / l[k];
-      T o[CW];
+    for (int i = 0; i < NE; ++i) o[i] = acc[i] * r;
+    T* orow = a.O + static_cast<size_t>(v) * a.F + off;
 #pragma unroll
-      for (int i = 0; i < CW; ++i) o[i] = acc[k][i] * r;
-      st_chunk(a.O + static_cast<size_t>(v) * a.F + off[k], o);
-      if ((c + k * LPE) % a.GD == 0)
-        st_stat(a.stats, static_cast<size_t>(v) * a.H + head[k], l[k] == T(0) ? ninf<T>() : m[k],
-                l[k] == T(0) ? T(0) : glog(l[k]));
+    for (int k = 0; k < CPL; ++k)
+      st_chunk<T, CB>(orow + k * CW, *reinterpret_cast<T(*)[CW]>(o + k * CW));
+    if (c % a.LPH == 0) {
+      T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + h);
+      rec[0] = l == T(0) ? ninf<T>() : m;
+      rec[1] = l == T(0) ? T(0) : lg2(l);
+      rec[2] = VAR == GF_DOT ? rk : erv;
     }
   }
 }
@@ -277,7 +240,7 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   for (int i = eb; i < ee; ++i) {
     const int u = __ldg(a.idx + i);
     if (lane < a.H) {
-      const T p = gexp(generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh) - m);
+      const T p = expd(generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh) - m);
       l += p;
       ph[lane] = p;
     }
@@ -288,8 +251,10 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   }
   if (lane < a.H) {
     lh[lane] = l;
-    st_stat(a.stats, static_cast<size_t>(v) * a.H + lane, l == T(0) ? ninf<T>() : m,
-            l == T(0) ? T(0) : glog(l));
+    T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + lane);
+    rec[0] = l == T(0) ? ninf<T>() : m;
+    rec[1] = l == T(0) ? T(0) : lg2(l);
+    rec[2] = VAR == GF_DOT ? rkh : erh;
   }
   __syncwarp();
   for (int f = lane; f < a.F; f += 32) {
@@ -299,7 +264,7 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
 }
 
 // P materialisation (reference ForwardContext::P, engine.hpp:29): recompute
-// p = exp(s - lse) per edge and head.  Only on explicit request.
+// p = exp(s - m - log l) per edge and head.  Only on explicit request.
 template <typename T, int VAR>
 __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __restrict__ P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -308,21 +273,20 @@ __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __re
   const int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
   T erh, rkh;
   generic_row_setup<T, VAR>(a, v, lane, nullptr, erh, rkh);
-  T m, ll;
-  ld_stat(a.stats, static_cast<size_t>(v) * a.H + lane, m, ll);
+  const Rec<T> r = ld_rec(a.stats, static_cast<size_t>(v) * a.H + lane);
   for (int i = eb; i < ee; ++i) {
     const int u = __ldg(a.idx + i);
     P[static_cast<size_t>(i) * a.H + lane] =
-        prob(generic_score<T, VAR>(a, u, v, lane, nullptr, erh, rkh), m, ll);
+        prob(generic_score<T, VAR>(a, u, v, lane, nullptr, erh, rkh), r);
   }
 }
 
-template <typename T, int LPE, int CPL>
+template <typename T, int CB, int LPE, int CPL>
 int launch_fast_fwd(const FwdArgs<T>& a, int variant, int blocks, cudaStream_t s) {
   if (variant == GF_DOT)
-    fwd_fast<T, LPE, CPL, GF_DOT><<<blocks, 256, 0, s>>>(a);
+    fwd_fast<T, CB, LPE, CPL, GF_DOT><<<blocks, 256, 0, s>>>(a);
   else
-    fwd_fast<T, LPE, CPL, GF_ADD><<<blocks, 256, 0, s>>>(a);
+    fwd_fast<T, CB, LPE, CPL, GF_ADD><<<blocks, 256, 0, s>>>(a);
   GF_CHECK_LAUNCH("fwd_fast");
   return GF_OK;
 }
@@ -331,46 +295,65 @@ int launch_fast_fwd(const FwdArgs<T>& a, int variant, int blocks, cudaStream_t s
 
 FastShape fast_shape(int H, int D, int elem_bytes) {
   FastShape f;
-  const int cw = 16 / elem_bytes;
-  if (H < 1 || D < 1 || D % cw) return f;
-  const int gd = D / cw;
-  const long chunks = static_cast<long>(H) * gd;
+  if (H < 1 || D < 1) return f;
+  const long row = static_cast<long>(D) * elem_bytes;
+  const int cb = row % 32 == 0 ? 32 : (row % 16 == 0 ? 16 : 0);
+  if (!cb) return f;
+  const long cph = row / cb;
   auto pow2 = [](long x) { return x > 0 && (x & (x - 1)) == 0; };
-  if (!pow2(gd) || !pow2(chunks) || chunks > 128) return f;
+  const int cpl = cph >= 2 ? 2 : 1;
+  if (cb == 16 && cpl != 1) return f;  // 16 B chunks only for one-chunk heads
+  const long lph = cph / cpl;
+  const long lpe = static_cast<long>(H) * lph;
+  if (!pow2(cph) || !pow2(lpe) || lpe > 32) return f;
   f.ok = true;
-  f.gd = gd;
-  f.lpe = chunks < 32 ? static_cast<int>(chunks) : 32;
-  f.cpl = static_cast<int>(chunks / f.lpe);
+  f.cb = cb;
+  f.cpl = cpl;
+  f.lph = static_cast<int>(lph);
+  f.lpe = static_cast<int>(lpe);
   return f;
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static bool aligned(const void* p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; }
 
 template <typename T>
 int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_t s) {
   if (g.n == 0) return GF_OK;
   FwdArgs<T> a = a0;
   const FastShape fs = fast_shape(a.H, a.D, sizeof(T));
-  const bool al = aligned16(a.V) && aligned16(a.O) &&
-                  (variant == GF_ADD || (aligned16(a.Q) && aligned16(a.K)));
-  if (fs.ok && al) {
-    a.GD = fs.gd;
+  const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
+  const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
+                  aligned(a.stats, 32) &&
+                  (variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
+  if (al) {
+    a.LPH = fs.lph;
     const int warp_rows = g.n - a.n_cta;
     const int blocks = a.n_cta + (warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    switch (fs.lpe * 8 + fs.cpl) {
-      case 1 * 8 + 1: return launch_fast_fwd<T, 1, 1>(a, variant, blocks, s);
-      case 2 * 8 + 1: return launch_fast_fwd<T, 2, 1>(a, variant, blocks, s);
-      case 4 * 8 + 1: return launch_fast_fwd<T, 4, 1>(a, variant, blocks, s);
-      case 8 * 8 + 1: return launch_fast_fwd<T, 8, 1>(a, variant, blocks, s);
-      case 16 * 8 + 1: return launch_fast_fwd<T, 16, 1>(a, variant, blocks, s);
-      case 32 * 8 + 1: return launch_fast_fwd<T, 32, 1>(a, variant, blocks, s);
-      case 32 * 8 + 2: return launch_fast_fwd<T, 32, 2>(a, variant, blocks, s);
-      case 32 * 8 + 4: return launch_fast_fwd<T, 32, 4>(a, variant, blocks, s);
+    const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;
+    switch (key) {
+      case 32011: return launch_fast_fwd<T, 32, 1, 1>(a, variant, blocks, s);
+      case 32021: return launch_fast_fwd<T, 32, 2, 1>(a, variant, blocks, s);
+      case 32041: return launch_fast_fwd<T, 32, 4, 1>(a, variant, blocks, s);
+      case 32081: return launch_fast_fwd<T, 32, 8, 1>(a, variant, blocks, s);
+      case 32161: return launch_fast_fwd<T, 32, 16, 1>(a, variant, blocks, s);
+      case 32321: return launch_fast_fwd<T, 32, 32, 1>(a, variant, blocks, s);
+      case 32012: return launch_fast_fwd<T, 32, 1, 2>(a, variant, blocks, s);
+      case 32022: return launch_fast_fwd<T, 32, 2, 2>(a, variant, blocks, s);
+      case 32042: return launch_fast_fwd<T, 32, 4, 2>(a, variant, blocks, s);
+      case 32082: return launch_fast_fwd<T, 32, 8, 2>(a, variant, blocks, s);
+      case 32162: return launch_fast_fwd<T, 32, 16, 2>(a, variant, blocks, s);
+      case 32322: return launch_fast_fwd<T, 32, 32, 2>(a, variant, blocks, s);
+      case 16011: return launch_fast_fwd<T, 16, 1, 1>(a, variant, blocks, s);
+      case 16021: return launch_fast_fwd<T, 16, 2, 1>(a, variant, blocks, s);
+      case 16041: return launch_fast_fwd<T, 16, 4, 1>(a, variant, blocks, s);
+      case 16081: return launch_fast_fwd<T, 16, 8, 1>(a, variant, blocks, s);
+      case 16161: return launch_fast_fwd<T, 16, 16, 1>(a, variant, blocks, s);
+      case 16321: return launch_fast_fwd<T, 16, 32, 1>(a, variant, blocks, s);
       default: break;
     }
   }
   if (a.H > 32) {
-    set_error("gf_attn_fwd: heads > 32 need a head shape that tiles into 16-byte chunks");
+    set_error("gf_attn_fwd: heads > 32 need a head shape that tiles into 16/32-byte chunks");
     return GF_ERR_UNSUPPORTED;
   }
   const size_t smem = static_cast<size_t>(kGenericWarps) * (2 * a.F + 64) * sizeof(T);

@@ -85,7 +85,7 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
   a.H = d.heads;
   a.D = d.head_dim;
   a.F = d.heads * d.head_dim;
-  a.GD = 1;
+  a.LPH = 1;
   a.l2 = d.l2;
   a.scale = static_cast<T>(d.scale);
   a.slope = static_cast<T>(d.slope);
@@ -108,14 +108,14 @@ int fwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
 
 template <typename T>
 int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, const void* V,
-             const void* O, const void* lse, const void* dO, void* dQ, void* dK, void* dV,
-             void* delta, int passes, cudaStream_t s) {
+             const void* O, void* stats, const void* dO, void* dQ, void* dK, void* dV, int passes,
+             cudaStream_t s) {
   gfb::BwdArgs<T> a{};
   a.n = g->n;
   a.H = d.heads;
   a.D = d.head_dim;
   a.F = d.heads * d.head_dim;
-  a.GD = 1;
+  a.LPH = 1;
   a.l2 = d.l2;
   a.scale = static_cast<T>(d.scale);
   a.slope = static_cast<T>(d.slope);
@@ -123,88 +123,77 @@ int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
   a.K = static_cast<const T*>(K);
   a.V = static_cast<const T*>(V);
   a.O = static_cast<const T*>(O);
-  a.stats = static_cast<const T*>(lse);
   a.dO = static_cast<const T*>(dO);
+  a.stats = static_cast<T*>(stats);
   a.dQ = static_cast<T*>(dQ);
   a.dK = static_cast<T*>(dK);
   a.dV = static_cast<T*>(dV);
-  if (delta) {
-    a.delta = static_cast<T*>(delta);
-  } else {
-    const size_t need = sizeof(T) * static_cast<size_t>(g->n) * d.heads;
-    if (g->scratch_bytes < need) {
-      cudaFree(g->scratch);
-      g->scratch = nullptr;
-      g->scratch_bytes = 0;
-      GF_CHECK_CUDA(cudaMalloc(&g->scratch, need));
-      g->scratch_bytes = need;
-    }
-    a.delta = static_cast<T*>(g->scratch);
-  }
   return gfb::launch_bwd<T>(*g, a, d.variant, passes, s);
+}
+
+bool bad_graph(gf_graph_t g, const char* who) {
+  if (g) return false;
+  gfb::set_error(std::string(who) + ": null graph");
+  return true;
 }
 
 }  // namespace
 
 extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                           const void* V, void* O, void* lse, void* P, void* stream) {
+                           const void* V, void* O, void* stats, void* P, void* stream) {
   if (int rc = check_desc(desc, "gf_attn_fwd")) return rc;
-  if (!g) {
-    gfb::set_error("gf_attn_fwd: null graph");
-    return GF_ERR_INVALID;
-  }
-  if (g->n > 0 && (!Q || !K || !V || !O || !lse)) {
+  if (bad_graph(g, "gf_attn_fwd")) return GF_ERR_INVALID;
+  if (g->n > 0 && (!Q || !K || !V || !O || !stats)) {
     gfb::set_error("gf_attn_fwd: null operand");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
-  return desc->dtype == GF_F32 ? fwd_impl<float>(g, *desc, Q, K, V, O, lse, P, s)
-                               : fwd_impl<double>(g, *desc, Q, K, V, O, lse, P, s);
+  return desc->dtype == GF_F32 ? fwd_impl<float>(g, *desc, Q, K, V, O, stats, P, s)
+                               : fwd_impl<double>(g, *desc, Q, K, V, O, stats, P, s);
 }
 
 extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
-                           const void* V, const void* O, const void* lse, const void* dO,
-                           void* dQ, void* dK, void* dV, void* delta, void* stream) {
+                           const void* V, const void* O, void* stats, const void* dO, void* dQ,
+                           void* dK, void* dV, void* stream) {
   if (int rc = check_desc(desc, "gf_attn_bwd")) return rc;
-  if (!g) {
-    gfb::set_error("gf_attn_bwd: null graph");
-    return GF_ERR_INVALID;
-  }
-  if (g->n > 0 && (!Q || !K || !V || !O || !lse || !dO || !dQ || !dK || !dV)) {
+  if (bad_graph(g, "gf_attn_bwd")) return GF_ERR_INVALID;
+  if (g->n > 0 && (!Q || !K || !V || !O || !stats || !dO || !dQ || !dK || !dV)) {
     gfb::set_error("gf_attn_bwd: null operand");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
-             ? bwd_impl<float>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, 3, s)
-             : bwd_impl<double>(g, *desc, Q, K, V, O, lse, dO, dQ, dK, dV, delta, 3, s);
+             ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, dQ, dK, dV, 3, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, O, stats, dO, dQ, dK, dV, 3, s);
 }
 
 extern "C" int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const void* Q,
-                                const void* K, const void* V, const void* O, const void* stats,
-                                const void* dO, void* dK, void* delta, void* stream) {
+                                const void* K, const void* V, const void* O, void* stats,
+                                const void* dO, void* dK, void* stream) {
   if (int rc = check_desc(desc, "gf_attn_bwd_rows")) return rc;
-  if (!g || (g->n > 0 && (!Q || !K || !V || !O || !stats || !dO || !dK || !delta))) {
-    gfb::set_error("gf_attn_bwd_rows: null graph or operand");
+  if (bad_graph(g, "gf_attn_bwd_rows")) return GF_ERR_INVALID;
+  if (g->n > 0 && (!Q || !K || !V || !O || !stats || !dO || !dK)) {
+    gfb::set_error("gf_attn_bwd_rows: null operand");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
-             ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, delta, 1, s)
-             : bwd_impl<double>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, delta, 1, s);
+             ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, 1, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, 1, s);
 }
 
 extern "C" int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q,
                                 const void* K, const void* V, const void* stats, const void* dO,
-                                const void* delta, void* dQ, void* dV, void* stream) {
+                                void* dQ, void* dV, void* stream) {
   if (int rc = check_desc(desc, "gf_attn_bwd_cols")) return rc;
-  if (!g || (g->n > 0 && (!Q || !K || !V || !stats || !dO || !delta || !dQ || !dV))) {
-    gfb::set_error("gf_attn_bwd_cols: null graph or operand");
+  if (bad_graph(g, "gf_attn_bwd_cols")) return GF_ERR_INVALID;
+  if (g->n > 0 && (!Q || !K || !V || !stats || !dO || !dQ || !dV)) {
+    gfb::set_error("gf_attn_bwd_cols: null operand");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
-  void* dl = const_cast<void*>(delta);
+  void* st = const_cast<void*>(stats);
   return desc->dtype == GF_F32
-             ? bwd_impl<float>(g, *desc, Q, K, V, nullptr, stats, dO, dQ, nullptr, dV, dl, 2, s)
-             : bwd_impl<double>(g, *desc, Q, K, V, nullptr, stats, dO, dQ, nullptr, dV, dl, 2, s);
+             ? bwd_impl<float>(g, *desc, Q, K, V, nullptr, st, dO, dQ, nullptr, dV, 2, s)
+             : bwd_impl<double>(g, *desc, Q, K, V, nullptr, st, dO, dQ, nullptr, dV, 2, s);
 }

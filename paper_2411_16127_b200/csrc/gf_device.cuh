@@ -8,16 +8,30 @@
 namespace gfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr float kLog2e = 1.4426950408889634f;
 
-// 16-byte chunk of T: 4 floats or 2 doubles.
-template <typename T>
+// ---------------------------------------------------------------- chunks --
+// A lane moves one CB-byte chunk per load: CB = 32 uses the sm_100 256-bit
+// global load (LDG.E.256, one full 32 B sector per lane), CB = 16 the 128-bit
+// one.  Gathered rows are read through the non-coherent path without L1
+// allocation (they are touched once per edge); owned rows use plain loads.
+template <typename T, int CB>
 struct Chunk {
-  static constexpr int W = 16 / sizeof(T);
+  static constexpr int W = CB / static_cast<int>(sizeof(T));
 };
 
-template <typename T>
-__device__ __forceinline__ void ld_chunk(const T* __restrict__ p, T (&x)[16 / sizeof(T)]) {
-  if constexpr (sizeof(T) == 4) {
+template <typename T, int CB>
+__device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
+  if constexpr (CB == 32 && sizeof(T) == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
+                   "=f"(x[6]), "=f"(x[7])
+                 : "l"(p));
+  } else if constexpr (CB == 32) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(p));
+  } else if constexpr (sizeof(T) == 4) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(p));
     x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
   } else {
@@ -26,48 +40,93 @@ __device__ __forceinline__ void ld_chunk(const T* __restrict__ p, T (&x)[16 / si
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void st_chunk(T* __restrict__ p, const T (&x)[16 / sizeof(T)]) {
+template <typename T, int CB>
+__device__ __forceinline__ void ld_own(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
+  constexpr int W = CB / sizeof(T);
   if constexpr (sizeof(T) == 4) {
-    *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + i);
+      x[i] = v.x, x[i + 1] = v.y, x[i + 2] = v.z, x[i + 3] = v.w;
+    }
   } else {
-    *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+#pragma unroll
+    for (int i = 0; i < W; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(p + i);
+      x[i] = v.x, x[i + 1] = v.y;
+    }
   }
 }
 
-// exp(x): one MUFU.EX2 plus a multiply for fp32, full precision for fp64.
-__device__ __forceinline__ float gexp(float x) { return exp2f(x * 1.4426950408889634f); }
-__device__ __forceinline__ double gexp(double x) { return exp(x); }
-__device__ __forceinline__ float glog(float x) { return logf(x); }
-__device__ __forceinline__ double glog(double x) { return log(x); }
+template <typename T, int CB>
+__device__ __forceinline__ void st_chunk(T* __restrict__ p, const T (&x)[CB / sizeof(T)]) {
+  constexpr int W = CB / sizeof(T);
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < W; i += 4)
+      *reinterpret_cast<float4*>(p + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; i += 2) *reinterpret_cast<double2*>(p + i) = make_double2(x[i], x[i + 1]);
+  }
+}
+
+// ------------------------------------------------------------------- exp --
+// ex2 on the SFU (one MUFU.EX2, flush-to-zero) for fp32; full precision fp64.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double ex2(double x) { return exp2(x); }
+__device__ __forceinline__ float lg2(float x) { return log2f(x); }
+__device__ __forceinline__ double lg2(double x) { return log2(x); }
+template <typename T>
+__device__ __forceinline__ T l2e() {
+  return static_cast<T>(1.4426950408889634073599246810019);
+}
+/// exp(d) for d = s - m computed first (keeps relative precision for any |s|).
+template <typename T>
+__device__ __forceinline__ T expd(T d) {
+  return ex2(d * l2e<T>());
+}
 
 template <typename T>
 __device__ __forceinline__ T ninf() {
   return -INFINITY;
 }
 
-// Softmax statistics per (row, head): (m, log l) with m the row max and l the
-// sum of exp(s - m).  p = exp((s - m) - log l) keeps full relative precision
-// for any score magnitude (a single fused lse = m + log l would lose
-// ulp(|m|) absolute, i.e. ~6e-5 relative at |s| ~ 1e3 in fp32).
+// ------------------------------------------------------ softmax records --
+// Per (row v, head h) record of 4 T, written by the forward and pass A and
+// gathered by pass B in ONE load:
+//   [0] m     row max of the scores (natural units)
+//   [1] ll2   log2 of l = sum exp(s - m)        => p = 2^((s - m) log2e - ll2)
+//   [2] aux   er[v,h] (GAT) | 1/max(||K[v,h]||,eps) (AGNN) | 0
+//   [3] delta <dO[v,h], O[v,h]> (written by backward pass A)
+// Splitting lse into (m, log l) keeps p exact-relative for any score
+// magnitude (a fused fp32 lse loses ulp(|m|), ~6e-5 at |s| ~ 1e3).
 template <typename T>
-__device__ __forceinline__ void ld_stat(const T* __restrict__ st, size_t i, T& m, T& ll) {
+struct Rec {
+  T m, ll2, aux, delta;
+};
+
+template <typename T>
+__device__ __forceinline__ Rec<T> ld_rec(const T* __restrict__ st, size_t i) {
+  Rec<T> r;
   if constexpr (sizeof(T) == 4) {
-    const float2 v = __ldg(reinterpret_cast<const float2*>(st) + i);
-    m = v.x, ll = v.y;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(st) + i);
+    r.m = v.x, r.ll2 = v.y, r.aux = v.z, r.delta = v.w;
   } else {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(st) + i);
-    m = v.x, ll = v.y;
+    double x[4];
+    ld_gather<double, 32>(st + 4 * i, x);
+    r.m = x[0], r.ll2 = x[1], r.aux = x[2], r.delta = x[3];
   }
+  return r;
 }
+
 template <typename T>
-__device__ __forceinline__ void st_stat(T* st, size_t i, T m, T ll) {
-  st[2 * i] = m;
-  st[2 * i + 1] = ll;
-}
-template <typename T>
-__device__ __forceinline__ T prob(T s, T m, T ll) {
-  return gexp((s - m) - ll);
+__device__ __forceinline__ T prob(T s, const Rec<T>& r) {
+  return ex2((s - r.m) * l2e<T>() - r.ll2);
 }
 
 template <typename T>
@@ -79,37 +138,12 @@ __device__ __forceinline__ T lrelu_grad(T pre, T slope) {
   return pre > T(0) ? T(1) : slope;  // autograd.hpp:113 (kink takes the slope)
 }
 
-// Sum of per-chunk partials over one head.  Lanes of an edge group (LPE
-// lanes, aligned) hold chunk c + k*LPE for k < CPL; a head spans GD
-// consecutive chunks (GD a power of two).  After the call every lane holds
-// its head's total in x[k].
-template <int LPE, int CPL, typename T>
-__device__ __forceinline__ void head_sum(T (&x)[CPL], int gd) {
-  const int lim = gd < LPE ? gd : LPE;
-#pragma unroll
-  for (int off = 1; off < LPE; off <<= 1) {
-    if (off < lim) {
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) x[k] += __shfl_xor_sync(kFull, x[k], off);
-    }
-  }
-  if constexpr (CPL > 1) {
-    if (gd > LPE) {
-      const int gk = gd / LPE;  // consecutive k per head
-      T t[CPL];
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        const int k0 = (k / gk) * gk;
-        T s = T(0);
-#pragma unroll
-        for (int j = 0; j < CPL; ++j)
-          if (j >= k0 && j < k0 + gk) s += x[j];
-        t[k] = s;
-      }
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) x[k] = t[k];
-    }
-  }
+/// Sum over the LPH lanes that share one head (aligned groups, LPH a power of
+/// two <= 32); every lane of the group ends with the total.
+template <typename T>
+__device__ __forceinline__ T head_sum(T x, int lph) {
+  for (int off = 1; off < lph; off <<= 1) x += __shfl_xor_sync(kFull, x, off);
+  return x;
 }
 
 template <typename T>
@@ -124,9 +158,6 @@ __device__ __forceinline__ T inv_norm(T sq) {
 // argument struct with Q, K, F, D, H, l2, scale, slope (FwdArgs / BwdArgs).
 constexpr int kGenericWarps = 4;
 
-// Score of edge u -> v for head h.  kvs: K[v] staged in shared memory (or
-// null to read global).  erh: er[v,h] (add).  rkh: 1/max(||K[v,h]||,eps)
-// (AGNN).  rq_out: 1/max(||Q[u,h]||,eps) (AGNN).  pre_out: el+er (add).
 template <typename T, int VAR, class A>
 __device__ __forceinline__ T generic_score(const A& a, int u, int v, int h, const T* kvs, T erh,
                                            T rkh, T* rq_out = nullptr, T* pre_out = nullptr) {
@@ -150,8 +181,7 @@ __device__ __forceinline__ T generic_score(const A& a, int u, int v, int h, cons
   }
 }
 
-// Per-row destination operands for lane h: er[v,h] (add) or the AGNN inverse
-// norm of K[v,h] (dot + l2).
+// Destination operands for lane h: er[v,h] (add) or 1/max(||K[v,h]||,eps).
 template <typename T, int VAR, class A>
 __device__ __forceinline__ void generic_row_setup(const A& a, int v, int lane, const T* kvs,
                                                   T& erh, T& rkh) {

@@ -122,7 +122,6 @@ void free_graph(DevGraph* g) {
   cudaFree(g->csc_row);
   cudaFree(g->row_order);
   cudaFree(g->col_order);
-  cudaFree(g->scratch);
   delete g;
 }
 

@@ -14,10 +14,6 @@ namespace gfb {
 // ------------------------------------------------------------------ errors --
 void set_error(const std::string& msg);
 
-struct Status {
-  int code = GF_OK;
-};
-
 #define GF_CHECK_CUDA(expr)                                                          \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \
@@ -54,28 +50,28 @@ struct DevGraph {
   int32_t n_cta_cols = 0, n_empty_cols = 0;
   int64_t max_in = 0, max_out = 0;
   int device = 0;
-  void* scratch = nullptr;  // delta for the backward when the caller passes none
-  size_t scratch_bytes = 0;
 };
 
 constexpr int kDefaultCtaThreshold = 1024;
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
 
 // ---------------------------------------------------------- kernel params --
+// Lane geometry of the fast path (see fast_shape): a lane owns CPL chunks of
+// CB bytes of ONE head; LPH lanes share a head; LPE = H * LPH lanes per edge.
 template <typename T>
 struct FwdArgs {
   const int32_t* ptr;    // CSR row pointer
   const int32_t* idx;    // CSR column (source) ids
   const int32_t* order;  // row schedule
   int n, n_cta;
-  int H, D, F, GD;  // GD = chunks per head (fast path)
+  int H, D, F, LPH;
   int l2;
   T scale, slope;
   const T* Q;  // dot: N x F; add: el N x H
   const T* K;  // dot: N x F; add: er N x H
   const T* V;
   T* O;
-  T* stats;  // N x H x 2: (row max, log sum-exp) per head
+  T* stats;  // N x H x 4 records (gf_device.cuh Rec)
 };
 
 template <typename T>
@@ -84,16 +80,15 @@ struct BwdArgs {
   const int32_t* idx;
   const int32_t* order;
   int n, n_cta;
-  int H, D, F, GD;
+  int H, D, F, LPH;
   int l2;
   T scale, slope;
   const T* Q;
   const T* K;
   const T* V;
   const T* O;
-  const T* stats;
   const T* dO;
-  T* delta;  // pass A writes, pass B reads
+  T* stats;  // records; pass A writes delta, pass B reads them
   T* dQ;     // pass B (dot) / del (add)
   T* dK;     // pass A (dot) / der (add)
   T* dV;     // pass B
@@ -109,11 +104,13 @@ int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T*
 template <typename T>
 int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStream_t s);
 
-// Fast-path eligibility: chunk = 16 bytes; D a multiple of the chunk width,
-// chunks per head a power of two, F/CW a power of two <= 128, 16 B alignment.
+// Fast-path geometry.  Chunk bytes CB: 32 when a head row is a multiple of
+// 32 B (256-bit loads), else 16.  Chunks per head CPH = D*sizeof(T)/CB; a lane
+// owns CPL = min(CPH, 2) chunks and LPH = CPH / CPL lanes share a head, so
+// lanes per edge LPE = H * LPH (a power of two <= 32).
 struct FastShape {
   bool ok = false;
-  int lpe = 0, cpl = 0, gd = 0;
+  int cb = 0, lpe = 0, cpl = 0, lph = 0;
 };
 FastShape fast_shape(int H, int D, int elem_bytes);
 

@@ -132,7 +132,7 @@ void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>
   const gf_attn_desc desc = make_desc<T>(kind, d);
   DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), dv = DevBuf::from(V.data);
   O.assign(static_cast<size_t>(g.num_nodes * d), T(0));
-  lse.assign(static_cast<size_t>(2 * g.num_nodes), T(0));  // (m, log l) per row
+  lse.assign(static_cast<size_t>(4 * g.num_nodes), T(0));  // softmax records (4 per row)
   DevBuf dO(sizeof(T) * O.size()), dl(sizeof(T) * lse.size());
   DevBuf dp(P ? sizeof(T) * static_cast<size_t>(g.num_edges) : 0);
   GFH_CALL(gf_attn_fwd(dg, &desc, dq.p, dk.p, dv.p, dO.p, dl.p, P ? dp.p : nullptr, nullptr));
@@ -205,7 +205,7 @@ GradBundle<T> device_backward(const Graph& g, const ForwardContext<T>& ctx,
   const FusionPlan& plan = ctx.plan;
   std::vector<T> O = ctx.O, lse = ctx.lse;
   if (O.size() != static_cast<size_t>(g.num_nodes * d) ||
-      lse.size() != static_cast<size_t>(2 * g.num_nodes))
+      lse.size() != static_cast<size_t>(4 * g.num_nodes))
     device_forward(g, plan, ctx.Q, ctx.K, V, ctx.kind, O, lse, static_cast<std::vector<T>*>(nullptr));  // hand-built ctx
   gf_graph_t dg = device_graph(g, plan);
   const gf_attn_desc desc = make_desc<T>(ctx.kind, d);
@@ -218,7 +218,7 @@ GradBundle<T> device_backward(const Graph& g, const ForwardContext<T>& ctx,
   gb.dV = DenseMatrix<T>(V.rows, V.cols);
   DevBuf gq(sizeof(T) * gb.dQ.data.size()), gk(sizeof(T) * gb.dK.data.size()),
       gv(sizeof(T) * gb.dV.data.size());
-  GFH_CALL(gf_attn_bwd(dg, &desc, dq.p, dk.p, dv.p, dob.p, dl.p, ddo.p, gq.p, gk.p, gv.p, nullptr,
+  GFH_CALL(gf_attn_bwd(dg, &desc, dq.p, dk.p, dv.p, dob.p, dl.p, ddo.p, gq.p, gk.p, gv.p,
                        nullptr));
   GFH_CALL(gf_stream_sync(nullptr));
   gq.to(gb.dQ.data);

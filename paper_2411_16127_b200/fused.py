@@ -128,13 +128,13 @@ def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, 
                  stream=None):
     """One fused launch; returns (O, stats) or (O, stats, P).
 
-    stats is N x H x 2: (row max, log sum-exp) per head; lse = m + log l."""
+    stats is N x H x 4 softmax records {m, log2 l, aux, delta} (gf_cuda.h)."""
     n = g.n
     dt = V.dtype
     if O is None:
         O = torch.empty(n, spec.F, dtype=dt, device=V.device)
     if stats is None:
-        stats = torch.empty(n, spec.heads, 2, dtype=dt, device=V.device)
+        stats = torch.empty(n, spec.heads, 4, dtype=dt, device=V.device)
     P = torch.empty(max(g.e, 1), spec.heads, dtype=dt, device=V.device) if want_p else None
     d = spec.desc(dt)
     check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats), _p(P),
@@ -143,12 +143,12 @@ def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, 
 
 
 def lse_of(stats):
-    """log-sum-exp per (row, head) from the (m, log l) statistics."""
-    return stats[..., 0] + stats[..., 1]
+    """log-sum-exp per (row, head) from the records: m + log2(l) * ln 2."""
+    return stats[..., 0] + stats[..., 1] * 0.6931471805599453
 
 
 def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, stats, dO, dQ=None, dK=None,
-                  dV=None, delta=None, stream=None):
+                  dV=None, stream=None):
     """Pass A (CSR) + pass B (CSC); returns (dQ|del, dK|der, dV)."""
     dt = V.dtype
     dev = V.device
@@ -160,22 +160,22 @@ def attn_backward(g: DeviceGraph, spec: AttnSpec, Q, K, V, O, stats, dO, dQ=None
         dV = torch.empty(g.n, spec.F, dtype=dt, device=dev)
     d = spec.desc(dt)
     check(lib().gf_attn_bwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats), _p(dO),
-                            _p(dQ), _p(dK), _p(dV), _p(delta), _stream(stream)), "gf_attn_bwd")
+                            _p(dQ), _p(dK), _p(dV), _stream(stream)), "gf_attn_bwd")
     return dQ, dK, dV
 
 
-def attn_backward_rows(g, spec, Q, K, V, O, stats, dO, dK, delta, stream=None):
-    """Pass A only: dK | der and delta (CSR rows)."""
+def attn_backward_rows(g, spec, Q, K, V, O, stats, dO, dK, stream=None):
+    """Pass A only: dK | der, and delta into the stats records (CSR rows)."""
     d = spec.desc(V.dtype)
     check(lib().gf_attn_bwd_rows(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats),
-                                 _p(dO), _p(dK), _p(delta), _stream(stream)), "gf_attn_bwd_rows")
+                                 _p(dO), _p(dK), _stream(stream)), "gf_attn_bwd_rows")
 
 
-def attn_backward_cols(g, spec, Q, K, V, stats, dO, delta, dQ, dV, stream=None):
-    """Pass B only: dQ | del and dV (CSC columns), reading pass A's delta."""
+def attn_backward_cols(g, spec, Q, K, V, stats, dO, dQ, dV, stream=None):
+    """Pass B only: dQ | del and dV (CSC columns), reading pass A's records."""
     d = spec.desc(V.dtype)
     check(lib().gf_attn_bwd_cols(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(stats), _p(dO),
-                                 _p(delta), _p(dQ), _p(dV), _stream(stream)), "gf_attn_bwd_cols")
+                                 _p(dQ), _p(dV), _stream(stream)), "gf_attn_bwd_cols")
 
 
 class FusedAttention(torch.autograd.Function):
