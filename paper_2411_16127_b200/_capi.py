@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgraphfuse_cuda.so")
+# GF_CUDA_LIB overrides the library path (used only to A/B kernel build
+# variants, scripts/build_variant.py); the default is the in-tree build.
+LIB_PATH = os.environ.get("GF_CUDA_LIB") or os.path.join(_HERE, "libgraphfuse_cuda.so")
 
 GF_OK = 0
 GF_F32, GF_F64 = 0, 1

@@ -82,11 +82,11 @@ __device__ __forceinline__ void warp_sum(T (&x)[NV]) {
 
 // ------------------------------------------------------------ pass A ------
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? 4 : 2;
+  constexpr int U = CPL == 1 ? GF_U_ROWS : GF_U2;
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPE, sub = lane / LPE;
@@ -140,9 +140,11 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
 #pragma unroll
   for (int j = 0; j < NA; ++j) acc[j] = T(0);
 
+  int nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
   for (int base = eb; base < ee; base += 32) {
     const int cnt = min(32, ee - base);
-    const int myu = lane < cnt ? __ldg(a.idx + base + lane) : 0;
+    const int myu = nxt;
+    nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
     for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
       bool ok[U];
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
         } else {
-          el[t] = __ldg(Qb + uu * qs);
+          el[t] = ld_node(Qb + uu * qs);
         }
       }
 #pragma unroll
@@ -220,11 +222,11 @@ __global__ void __launch_bounds__(256) bwd_rows_fast(const BwdArgs<T> a) {
 
 // ------------------------------------------------------------ pass B ------
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256) bwd_cols_fast(const BwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? 4 : 2;
+  constexpr int U = CPL == 1 ? GF_U_COLS : GF_U2;
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPE, sub = lane / LPE;
@@ -271,9 +273,11 @@ __global__ void __launch_bounds__(256) bwd_cols_fast(const BwdArgs<T> a) {
 #pragma unroll
   for (int j = 0; j < NT; ++j) all[j] = T(0);
 
+  int nxt = sb + lane < se ? ld_idx(a.idx + sb + lane) : 0;
   for (int base = sb; base < se; base += 32) {
     const int cnt = min(32, se - base);
-    const int myv = lane < cnt ? __ldg(a.idx + base + lane) : 0;
+    const int myv = nxt;
+    nxt = base + 32 + lane < se ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
     for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
       bool ok[U];

@@ -38,11 +38,11 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
 }
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? 4 : 2;
+  constexpr int U = CPL == 1 ? GF_U_FWD : GF_U2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPE, sub = lane / LPE;
   const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
@@ -85,9 +85,11 @@ __global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
 #pragma unroll
   for (int i = 0; i < NE; ++i) acc[i] = T(0);
 
+  int nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
   for (int base = eb; base < ee; base += 32) {
     const int cnt = min(32, ee - base);
-    const int myu = lane < cnt ? __ldg(a.idx + base + lane) : 0;
+    const int myu = nxt;  // ids of this 32-edge chunk; prefetch the next one
+    nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
     for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
       bool ok[U];
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(256) fwd_fast(const FwdArgs<T> a) {
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
         } else {
-          s[t] = __ldg(Qb + uu * qs);
+          s[t] = ld_node(Qb + uu * qs);
         }
       }
       T smax = ninf<T>();

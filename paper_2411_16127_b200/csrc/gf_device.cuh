@@ -20,20 +20,85 @@ struct Chunk {
   static constexpr int W = CB / static_cast<int>(sizeof(T));
 };
 
+// L2 residency policy: the gathered node tables (V, Q|el, dO, K, records;
+// tens of MB) are marked evict_last so the streamed topology (neighbour ids,
+// hundreds of MB, read once per pass) marked evict_first does not push them
+// out of the 126 MB L2.
+#ifndef GF_L2HINT
+#define GF_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t pol_keep() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_stream() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+/// Streamed neighbour id (read once per pass).
+__device__ __forceinline__ int ld_idx(const int32_t* __restrict__ p) {
+#if GF_L2HINT
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(pol_stream()));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
+/// Gathered scalar of a node table (el[src], ...).
+template <typename T>
+__device__ __forceinline__ T ld_node(const T* __restrict__ p) {
+#if GF_L2HINT
+  T v;
+  if constexpr (sizeof(T) == 4)
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_keep()));
+  else
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_keep()));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
   if constexpr (CB == 32 && sizeof(T) == 4) {
+#if GF_L2HINT
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
+                   "=f"(x[6]), "=f"(x[7])
+                 : "l"(p), "l"(pol_keep()));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
                    "=f"(x[6]), "=f"(x[7])
                  : "l"(p));
+#endif
   } else if constexpr (CB == 32) {
+#if GF_L2HINT
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(p), "l"(pol_keep()));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
                  : "l"(p));
+#endif
   } else if constexpr (sizeof(T) == 4) {
+#if GF_L2HINT
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                 : "l"(p), "l"(pol_keep()));
+#else
     const float4 v = __ldg(reinterpret_cast<const float4*>(p));
     x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+#endif
   } else {
     const double2 v = __ldg(reinterpret_cast<const double2*>(p));
     x[0] = v.x, x[1] = v.y;
@@ -114,8 +179,9 @@ template <typename T>
 __device__ __forceinline__ Rec<T> ld_rec(const T* __restrict__ st, size_t i) {
   Rec<T> r;
   if constexpr (sizeof(T) == 4) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(st) + i);
-    r.m = v.x, r.ll2 = v.y, r.aux = v.z, r.delta = v.w;
+    float x[4];
+    ld_gather<float, 16>(st + 4 * i, x);
+    r.m = x[0], r.ll2 = x[1], r.aux = x[2], r.delta = x[3];
   } else {
     double x[4];
     ld_gather<double, 32>(st + 4 * i, x);

@@ -52,6 +52,37 @@ struct DevGraph {
   int device = 0;
 };
 
+// Occupancy vs memory-level parallelism of the latency-bound gathers, per
+// kernel: MINB = minimum resident 256-thread CTAs per SM requested from ptxas
+// (register cap 65536 / (256 * MINB)), U = edges in flight per lane.  Tuned
+// on B200 with scripts/ab_variants.sh (profiles/README.md): one-chunk lanes
+// (GAT 8x8) fwd/pass A MINB 3, U 4; pass B MINB 4, U 2; two-chunk lanes
+// (GT 8x16) MINB 2, U 1 for all three.
+#ifndef GF_MINB_FWD
+#define GF_MINB_FWD 3
+#endif
+#ifndef GF_U_FWD
+#define GF_U_FWD 4
+#endif
+#ifndef GF_MINB_ROWS
+#define GF_MINB_ROWS 3
+#endif
+#ifndef GF_U_ROWS
+#define GF_U_ROWS 4
+#endif
+#ifndef GF_MINB_COLS
+#define GF_MINB_COLS 4
+#endif
+#ifndef GF_U_COLS
+#define GF_U_COLS 2
+#endif
+#ifndef GF_MINB2
+#define GF_MINB2 2
+#endif
+#ifndef GF_U2
+#define GF_U2 1
+#endif
+
 constexpr int kDefaultCtaThreshold = 1024;
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
 
