@@ -131,6 +131,32 @@ def main():
                                         np.int64)
         carr[f"{name}/graph"] = np.array(gname)
     np.savez_compressed(os.path.join(OUT, "counters.npz"), **carr)
+
+    # Layer level (models.hpp:104-158), single head, f64: conv_forward +
+    # conv_backward of the reference on seeded X / weights / dO.
+    conv = {}
+    for mi, model in enumerate(("gt", "agnn", "gat")):
+        g = refs["rand40"]
+        rng = np.random.default_rng(100 + mi)
+        d_in, dim = 5, 4
+        X = rng.uniform(-1, 1, (g.n, d_in))
+        lim = 1 / np.sqrt(d_in)
+        Wq, Wk, Wv = (rng.uniform(-lim, lim, (d_in, dim)) for _ in range(3))
+        al, ar = rng.uniform(-lim, lim, (dim, 1)), rng.uniform(-lim, lim, (dim, 1))
+        dO = rng.uniform(-1, 1, (g.n, dim))
+        O = np.zeros((g.n, dim))
+        dWq, dWk, dWv = np.zeros((d_in, dim)), np.zeros((d_in, dim)), np.zeros((d_in, dim))
+        dal, dar = np.zeros((dim, 1)), np.zeros((dim, 1))
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        rc = oracle.ref().gfref_conv_f64(g.h, mi, dim, d_in, 0.0, 0.2, P(X), P(Wq), P(Wk), P(Wv),
+                                         P(al), P(ar), P(dO), P(O), P(dWq), P(dWk), P(dWv),
+                                         P(dal), P(dar))
+        assert rc == 0, oracle.ref().gfref_last_error()
+        for k, v in (("X", X), ("Wq", Wq), ("Wk", Wk), ("Wv", Wv), ("al", al), ("ar", ar),
+                     ("dO", dO), ("O", O), ("dWq", dWq), ("dWk", dWk), ("dWv", dWv),
+                     ("dal", dal), ("dar", dar)):
+            conv[f"{model}/{k}"] = v
+    np.savez_compressed(os.path.join(OUT, "conv.npz"), **conv)
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
