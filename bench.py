@@ -20,9 +20,11 @@ sources) timed on this host on a bounded sample (one head, a row slice).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config c4|c1|c2|c3|c5gat|c5gt]
 
-N>1 (torchrun): destination rows are sharded by edge count across ranks
-(weak scaling: every rank processes its edge-balanced row shard of the SAME
-graph; value = all edges / max-over-ranks time).
+N>1 (torchrun): nodes are sharded into contiguous ranges balanced by in+out
+edges (paper_2411_16127_b200/shard.py); each rank runs the three kernels on
+its rows / columns and the step includes the two NCCL all-gathers (source
+rows before the forward, dO + softmax records before pass B).  The graph is
+fixed as N grows (strong scaling); value = all edges / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -144,7 +146,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                 "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -259,14 +261,16 @@ def cpu_reference_sample(sub, layer, D, steps=1, seed=0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-frac", type=float, default=0.125,
+    ap.add_argument("--cpu-frac", type=float, default=0.5,
                     help="edge fraction of the CPU-baseline row slice")
     ap.add_argument("--cta-threshold", type=int, default=0)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -336,77 +340,105 @@ def run_ours(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.force_shard
+    if sharded:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     # ---- graph (setup, untimed): device generator -> device from_coo -> schedules
     n, src, dst = gen_graph_device(graph, dev)
     row_ptr, col, csc_ptr, csc_row, _ = fused.from_coo_device(n, src, dst)
     del src, dst
     e = int(col.numel())
-    shard = None
-    if world > 1:
-        from paper_2411_16127_b200 import shard as sh
-
-        shard = sh.RowShard.build(n, row_ptr, col, rank, world)
-        dg = shard.device_graph(cta_threshold=args.cta_threshold)
-    else:
-        dg = fused.DeviceGraph.from_device_csr(n, row_ptr, col, csc_ptr, csc_row,
-                                               cta_threshold=args.cta_threshold)
     spec = fused.AttnSpec("add" if layer == "gat" else "dot", H, D,
                           scale=(1.0 / np.sqrt(D)) if layer == "gt" else 1.0, slope=0.2,
                           l2=layer == "agnn")
     F = H * D
     qk = spec.qk_width
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234)
+    gen.manual_seed(1234)  # every rank draws the same global tables
 
     def u(*shape, amp=1.0):
         return (torch.rand(*shape, device=dev, generator=gen) * 2 - 1) * amp
 
     amp = 2.0 if layer == "gat" else 1.0
     Q, K, V, dO = u(n, qk, amp=amp), u(n, qk, amp=amp), u(n, F), u(n, F)
-    O = torch.empty(n, F, device=dev)
-    stats = torch.empty(n, H, 4, device=dev)
-    dQ, dK, dV = torch.empty(n, qk, device=dev), torch.empty(n, qk, device=dev), torch.empty(n, F, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream()
+    shard = None
+    if sharded:
+        # Row-sharded (paper_2411_16127_b200/shard.py): padded id space, this
+        # rank's block of every node table is its own nodes' rows.
+        from paper_2411_16127_b200.shard import RowShard, all_gather_rows
+
+        shard = RowShard.build(n, row_ptr, col, csc_ptr, csc_row, rank, world)
+        dg = shard.device_graph(cta_threshold=args.cta_threshold)
+        Q, K, V, dO = (shard.to_padded(x) for x in (Q, K, V, dO))
+        n_tab = shard.n_padded
+    else:
+        dg = fused.DeviceGraph.from_device_csr(n, row_ptr, col, csc_ptr, csc_row,
+                                               cta_threshold=args.cta_threshold)
+        n_tab = n
+    need_cpu = rank == 0 and not sharded and not args.no_cpu_baseline
+    host_rp = row_ptr.cpu().numpy() if need_cpu else None
+    host_col = col.cpu().numpy() if need_cpu else None
+    del row_ptr, col, csc_ptr, csc_row
+    O = torch.zeros(n_tab, F, device=dev)
+    stats = torch.zeros(n_tab, H, 4, device=dev)
+    dQ, dK, dV = (torch.zeros(n_tab, qk, device=dev), torch.zeros(n_tab, qk, device=dev),
+                  torch.zeros(n_tab, F, device=dev))
+    NEV = 6 if sharded else 4
 
     def step(ev=None):
-        if ev:
-            ev[0].record(stream)
+        rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
+        k = 0
+        rec(k)
+        if sharded:  # exchange 1: source-side projected rows (V, Q|el, and K for pass B)
+            for t in (V, Q) + ((K,) if layer != "gat" else ()):
+                all_gather_rows(t, shard)
+            k += 1
+            rec(k)
         fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream)
-        if ev:
-            ev[1].record(stream)
+        k += 1
+        rec(k)
         fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK, stream=stream)
-        if ev:
-            ev[2].record(stream)
+        k += 1
+        rec(k)
+        if sharded:  # exchange 2: dO and the softmax records of destination rows
+            all_gather_rows(dO, shard)
+            all_gather_rows(stats, shard)
+            k += 1
+            rec(k)
         fused.attn_backward_cols(dg, spec, Q, K, V, stats, dO, dQ, dV, stream=stream)
-        if ev:
-            ev[3].record(stream)
+        k += 1
+        rec(k)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NEV)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        if world > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.zero_()
             step(evs[i])
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-    k_fwd = [a[0].elapsed_time(a[1]) for a in evs]
-    k_ra = [a[1].elapsed_time(a[2]) for a in evs]
-    k_rb = [a[2].elapsed_time(a[3]) for a in evs]
-    tot = [a + b + c for a, b, c in zip(k_fwd, k_ra, k_rb)]
+    seg = [[a[j].elapsed_time(a[j + 1]) for a in evs] for j in range(NEV - 1)]
+    if sharded:
+        k_ag1, k_fwd, k_ra, k_ag2, k_rb = seg
+    else:
+        k_fwd, k_ra, k_rb = seg
+        k_ag1 = k_ag2 = [0.0]
+    tot = [evs[i][0].elapsed_time(evs[i][NEV - 1]) for i in range(args.steps)]
     sum_ms = sum(tot)
-    if world > 1:
+    if sharded:
         t = torch.tensor([sum_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         sum_ms = float(t.item())
@@ -415,7 +447,7 @@ def run_ours(args, rank, world):
 
     # ---- e2e through the C-ABI with pinned host buffers
     e2e_val, h2d, d2h = None, 0, 0
-    if world == 1:
+    if not sharded:
         hQ, hK, hV, hdO = [x.cpu().pin_memory() for x in (Q, K, V, dO)]
         hO, hdQ, hdK, hdV = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (O, dQ, dK, dV)]
         h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hdO))
@@ -446,20 +478,21 @@ def run_ours(args, rank, world):
     means = {"fwd": statistics.mean(k_fwd), "bwd_rows": statistics.mean(k_ra),
              "bwd_cols": statistics.mean(k_rb)}
     dom = max(means, key=means.get)
-    nb = dg.n
-    ab = algorithmic_bytes(dom, layer, nb, dg.e, H, D)
+    # per-launch algorithmic bytes of THIS rank's launches (owned nodes / edges)
+    nb = (shard.hi - shard.lo) if sharded else n
+    e_of = {"fwd": dg.e, "bwd_rows": dg.e,
+            "bwd_cols": int(shard.csc_row.numel()) if sharded else dg.e}
+    ab = algorithmic_bytes(dom, layer, nb, e_of[dom], H, D)
     achieved = ab / (means[dom] / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = ncu_traffic(args.config, dom)
-    step_bytes = sum(algorithmic_bytes(k, layer, nb, dg.e, H, D) for k in means)
+    step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D) for k in means)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if need_cpu:
         try:
-            rp = row_ptr.cpu().numpy()
-            cl = col.cpu().numpy()
             t0 = time.time()
-            sub = row_slice_sample(n, rp, cl, args.cpu_frac)
+            sub = row_slice_sample(n, host_rp, host_col, args.cpu_frac)
             times, es = cpu_reference_sample(sub, layer, D, steps=1)
             cpu_v = es / (times[0] * H) / 1e9
             cpu = {"value": cpu_v, "unit": "GEdges/s", "cores": os.cpu_count(),
@@ -477,14 +510,16 @@ def run_ours(args, rank, world):
         out = {
             "metric": "fused AT-GNN layer fwd+bwd GEdges/s", "value": value, "unit": "GEdges/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "nodes": n, "edges": e, "heads": H, "head_dim": D,
                        "max_in_degree": int(info.max_in_degree),
                        "cta_rows": int(info.n_cta_rows), "cta_threshold": int(info.cta_threshold),
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": f"row-sharded x{world} (NCCL all-gather)" if sharded else "1 GPU"},
             "kernels_ms": {k: round(v, 4) for k, v in means.items()},
+            "allgather_ms": ({"src_rows": round(statistics.mean(k_ag1), 4),
+                              "dO_records": round(statistics.mean(k_ag2), 4)} if sharded else None),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes": ab},
@@ -498,7 +533,7 @@ def run_ours(args, rank, world):
             "clocks": clk.summary(),
         }
         print(json.dumps(out))
-    if world > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
     return 0
 

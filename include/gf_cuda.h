@@ -107,6 +107,16 @@ int gf_graph_create_device(int64_t num_nodes, int64_t num_edges, const int32_t* 
                            const int32_t* d_col_idx, const int32_t* d_csc_ptr,
                            const int32_t* d_csc_row, int32_t cta_threshold, void* stream,
                            gf_graph_t* out);
+/* Row-sharded graph (multi-GPU, §8(e)): the CSR (rows this rank owns, e_csr
+ * edges) and the CSC (columns this rank owns, e_csc edges) may hold different
+ * edge sets of the same node-id space.  flags & GF_GRAPH_SKIP_EMPTY: rows /
+ * columns without edges are not visited at all (their outputs are left
+ * untouched) — used when most rows belong to other ranks. */
+#define GF_GRAPH_SKIP_EMPTY 1
+int gf_graph_create_split(int64_t num_nodes, int64_t e_csr, const int32_t* d_row_ptr,
+                          const int32_t* d_col_idx, int64_t e_csc, const int32_t* d_csc_ptr,
+                          const int32_t* d_csc_row, int32_t cta_threshold, int32_t flags,
+                          void* stream, gf_graph_t* out);
 /* Device from_coo (graph.cpp:61-78): sort by (dst, src), reject ids out of
  * range (GF_ERR_GRAPH, *bad = input edge index) and duplicates (GF_ERR_GRAPH,
  * *bad = -2 - sorted position), build CSR and CSC (+ csc_edge_perm) bit-exact

@@ -48,6 +48,8 @@ SIGNATURES = {
                                   C.POINTER(_vp)]),
     "gf_graph_create_device": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32,
                                          _vp, C.POINTER(_vp)]),
+    "gf_graph_create_split": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp,
+                                        C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
     "gf_from_coo_device": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      C.POINTER(C.c_int64), _vp]),
     "gf_graph_destroy": (C.c_int, [_vp]),

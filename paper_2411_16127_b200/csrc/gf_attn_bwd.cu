@@ -566,6 +566,8 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   BwdArgs<T> ra = a, ca = a;
   ra.ptr = g.row_ptr, ra.idx = g.col, ra.order = g.row_order, ra.n_cta = g.n_cta_rows;
   ca.ptr = g.csc_ptr, ca.idx = g.csc_row, ca.order = g.col_order, ca.n_cta = g.n_cta_cols;
+  ra.n = g.active_rows();
+  ca.n = g.active_cols();
   const bool do_a = passes & 1, do_b = passes & 2;
   const bool dot = variant == GF_DOT;
   // Each pass picks the fast path independently (both paths use the same
@@ -579,8 +581,8 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   const bool fast_b = base && aligned(a.V, 16) && aligned(a.dO, cb) && aligned(a.dV, 16) &&
                       (!dot || (aligned(a.Q, 16) && aligned(a.K, cb) && aligned(a.dQ, 16)));
   ra.LPH = ca.LPH = fs.ok ? fs.lph : 1;
-  const int rb = (do_a && fast_a) ? ra.n_cta + (g.n - ra.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
-  const int cbk = (do_b && fast_b) ? ca.n_cta + (g.n - ca.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+  const int rb = (do_a && fast_a) ? ra.n_cta + (ra.n - ra.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+  const int cbk = (do_b && fast_b) ? ca.n_cta + (ca.n - ca.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
   if (rb || cbk) {
     int rc = GF_OK;
     switch (fs.cb * 1000 + fs.lpe * 10 + fs.cpl) {
@@ -606,7 +608,7 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
     }
     if (rc) return rc;
   }
-  const bool gen_a = do_a && !fast_a, gen_b = do_b && !fast_b;
+  const bool gen_a = do_a && !fast_a && ra.n > 0, gen_b = do_b && !fast_b && ca.n > 0;
   if (!gen_a && !gen_b) return GF_OK;
   if (a.H > 32) {
     set_error("gf_attn_bwd: heads > 32 need a head shape that tiles into 16/32-byte chunks");
@@ -618,28 +620,29 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
     set_error("gf_attn_bwd: feature width too large for the generic path");
     return GF_ERR_UNSUPPORTED;
   }
-  const int blocks = (g.n + kGenericWarps - 1) / kGenericWarps;
+  const int rblk = (ra.n + kGenericWarps - 1) / kGenericWarps;
+  const int cblk = (ca.n + kGenericWarps - 1) / kGenericWarps;
   int rc;
   if (dot) {
     if (gen_a) {
       if ((rc = set_smem(bwd_rows_generic<T, GF_DOT>, sa))) return rc;
-      bwd_rows_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
+      bwd_rows_generic<T, GF_DOT><<<rblk, 32 * kGenericWarps, sa, s>>>(ra);
       GF_CHECK_LAUNCH("bwd_rows_generic");
     }
     if (gen_b) {
       if ((rc = set_smem(bwd_cols_generic<T, GF_DOT>, sbm))) return rc;
-      bwd_cols_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, sbm, s>>>(ca);
+      bwd_cols_generic<T, GF_DOT><<<cblk, 32 * kGenericWarps, sbm, s>>>(ca);
       GF_CHECK_LAUNCH("bwd_cols_generic");
     }
   } else {
     if (gen_a) {
       if ((rc = set_smem(bwd_rows_generic<T, GF_ADD>, sa))) return rc;
-      bwd_rows_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sa, s>>>(ra);
+      bwd_rows_generic<T, GF_ADD><<<rblk, 32 * kGenericWarps, sa, s>>>(ra);
       GF_CHECK_LAUNCH("bwd_rows_generic");
     }
     if (gen_b) {
       if ((rc = set_smem(bwd_cols_generic<T, GF_ADD>, sbm))) return rc;
-      bwd_cols_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, sbm, s>>>(ca);
+      bwd_cols_generic<T, GF_ADD><<<cblk, 32 * kGenericWarps, sbm, s>>>(ca);
       GF_CHECK_LAUNCH("bwd_cols_generic");
     }
   }

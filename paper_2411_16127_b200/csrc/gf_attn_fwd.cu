@@ -322,6 +322,7 @@ template <typename T>
 int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_t s) {
   if (g.n == 0) return GF_OK;
   FwdArgs<T> a = a0;
+  if (a.n == 0) return GF_OK;  // every row skipped (row-sharded graph)
   const FastShape fs = fast_shape(a.H, a.D, sizeof(T));
   const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
   const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
@@ -329,7 +330,7 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_
                   (variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
   if (al) {
     a.LPH = fs.lph;
-    const int warp_rows = g.n - a.n_cta;
+    const int warp_rows = a.n - a.n_cta;
     const int blocks = a.n_cta + (warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;
     switch (key) {
@@ -363,7 +364,7 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_
     set_error("gf_attn_fwd: feature width too large for the generic path");
     return GF_ERR_UNSUPPORTED;
   }
-  const int blocks = (g.n + kGenericWarps - 1) / kGenericWarps;
+  const int blocks = (a.n + kGenericWarps - 1) / kGenericWarps;
   if (variant == GF_DOT) {
     if (smem > 48 * 1024)
       GF_CHECK_CUDA(cudaFuncSetAttribute(fwd_generic<T, GF_DOT>,

@@ -182,40 +182,55 @@ __global__ void csc_perm_kernel(const uint64_t* __restrict__ k_ds, const uint64_
 using gfb::DevGraph;
 
 
-extern "C" int gf_graph_create_device(int64_t n, int64_t e, const int32_t* d_row_ptr,
-                                      const int32_t* d_col, const int32_t* d_csc_ptr,
-                                      const int32_t* d_csc_row, int32_t cta_threshold,
-                                      void* stream, gf_graph_t* out) {
-  if (!out || n < 0 || e < 0 || n >= (1LL << 31) - 1 || e >= (1LL << 31) - 1) {
-    gfb::set_error("gf_graph_create_device: invalid sizes (int32 node/edge ids required)");
+extern "C" int gf_graph_create_split(int64_t n, int64_t e_csr, const int32_t* d_row_ptr,
+                                     const int32_t* d_col, int64_t e_csc,
+                                     const int32_t* d_csc_ptr, const int32_t* d_csc_row,
+                                     int32_t cta_threshold, int32_t flags, void* stream,
+                                     gf_graph_t* out) {
+  constexpr int64_t kMax = (1LL << 31) - 1;
+  if (!out || n < 0 || e_csr < 0 || e_csc < 0 || n >= kMax || e_csr >= kMax || e_csc >= kMax) {
+    gfb::set_error("gf_graph_create: invalid sizes (int32 node/edge ids required)");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
   auto* g = new gf_graph_s();
   g->n = static_cast<int32_t>(n);
-  g->e = static_cast<int32_t>(e);
-  const size_t np = sizeof(int32_t) * (n + 1), ep = sizeof(int32_t) * (e > 0 ? e : 1);
+  g->e = static_cast<int32_t>(e_csr);
+  g->e_csc = static_cast<int32_t>(e_csc);
+  g->skip_empty = (flags & GF_GRAPH_SKIP_EMPTY) != 0;
+  const size_t np = sizeof(int32_t) * (n + 1);
+  const size_t er = sizeof(int32_t) * (e_csr > 0 ? e_csr : 1);
+  const size_t ec = sizeof(int32_t) * (e_csc > 0 ? e_csc : 1);
   auto fail = [&](int rc) {
     gfb::free_graph(g);
     return rc;
   };
-  if (cudaMalloc(&g->row_ptr, np) || cudaMalloc(&g->col, ep) || cudaMalloc(&g->csc_ptr, np) ||
-      cudaMalloc(&g->csc_row, ep)) {
-    gfb::set_error("gf_graph_create_device: cudaMalloc failed");
+  if (cudaMalloc(&g->row_ptr, np) || cudaMalloc(&g->col, er) || cudaMalloc(&g->csc_ptr, np) ||
+      cudaMalloc(&g->csc_row, ec)) {
+    gfb::set_error("gf_graph_create: cudaMalloc failed");
     return fail(GF_ERR_CUDA);
   }
   if (cudaMemcpyAsync(g->row_ptr, d_row_ptr, np, cudaMemcpyDeviceToDevice, s) ||
       cudaMemcpyAsync(g->csc_ptr, d_csc_ptr, np, cudaMemcpyDeviceToDevice, s) ||
-      (e > 0 && cudaMemcpyAsync(g->col, d_col, sizeof(int32_t) * e, cudaMemcpyDeviceToDevice, s)) ||
-      (e > 0 &&
-       cudaMemcpyAsync(g->csc_row, d_csc_row, sizeof(int32_t) * e, cudaMemcpyDeviceToDevice, s))) {
-    gfb::set_error("gf_graph_create_device: copy failed");
+      (e_csr > 0 &&
+       cudaMemcpyAsync(g->col, d_col, sizeof(int32_t) * e_csr, cudaMemcpyDeviceToDevice, s)) ||
+      (e_csc > 0 && cudaMemcpyAsync(g->csc_row, d_csc_row, sizeof(int32_t) * e_csc,
+                                    cudaMemcpyDeviceToDevice, s))) {
+    gfb::set_error("gf_graph_create: copy failed");
     return fail(GF_ERR_CUDA);
   }
   int rc = gfb::finish_graph(g, cta_threshold, s);
   if (rc) return fail(rc);
   *out = g;
   return GF_OK;
+}
+
+extern "C" int gf_graph_create_device(int64_t n, int64_t e, const int32_t* d_row_ptr,
+                                      const int32_t* d_col, const int32_t* d_csc_ptr,
+                                      const int32_t* d_csc_row, int32_t cta_threshold,
+                                      void* stream, gf_graph_t* out) {
+  return gf_graph_create_split(n, e, d_row_ptr, d_col, e, d_csc_ptr, d_csc_row, cta_threshold, 0,
+                               stream, out);
 }
 
 extern "C" int gf_graph_create(int64_t n, int64_t e, const int64_t* row_ptr,

@@ -50,6 +50,11 @@ struct DevGraph {
   int32_t n_cta_cols = 0, n_empty_cols = 0;
   int64_t max_in = 0, max_out = 0;
   int device = 0;
+  int32_t e_csc = 0;        // CSC edge count (== e unless row-sharded)
+  bool skip_empty = false;  // do not visit rows / columns without edges
+  /// Rows (resp. columns) a pass visits: the empty ones trail the order.
+  int32_t active_rows() const { return skip_empty ? n - n_empty_rows : n; }
+  int32_t active_cols() const { return skip_empty ? n - n_empty_cols : n; }
 };
 
 // Occupancy vs memory-level parallelism of the latency-bound gathers, per

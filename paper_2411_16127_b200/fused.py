@@ -82,6 +82,17 @@ class DeviceGraph:
               "gf_graph_create_device")
         return cls(h)
 
+    @classmethod
+    def from_split(cls, n, row_ptr, col, csc_ptr, csc_row, cta_threshold=0, skip_empty=False,
+                   stream=None):
+        """CSR and CSC with different edge sets (row-sharded graph, shard.py)."""
+        rp, c, cp, cr = [t.to(torch.int32).contiguous() for t in (row_ptr, col, csc_ptr, csc_row)]
+        h = C.c_void_p()
+        check(lib().gf_graph_create_split(int(n), int(c.numel()), _p(rp), _p(c), int(cr.numel()),
+                                          _p(cp), _p(cr), int(cta_threshold), int(skip_empty),
+                                          _stream(stream), C.byref(h)), "gf_graph_create_split")
+        return cls(h)
+
     def schedule(self):
         """(row_order, col_order) as int32 numpy arrays (degree-descending)."""
         ro = np.zeros(max(self.n, 1), np.int32)

@@ -1,0 +1,127 @@
+"""Row-sharded multi-GPU execution of the fused layer.
+
+Partition: contiguous node ranges balanced by in+out edge count; rank k owns
+nodes [b_k, b_{k+1}): the in-edges of its nodes (CSR rows: forward and
+backward pass A) and the out-edges of its nodes (CSC columns: pass B),
+owner-computes on both sides, no atomics, no reduce-scatter.
+
+Id space: nodes are relabelled new(v) = k*R + (v - b_k) with R = max shard
+size, so every rank's node slice is one contiguous block of a padded table of
+world*R rows.  NCCL all-gathers of per-rank slices then land in place
+(all_gather_into_tensor with the rank's block as input), and because the
+relabelling is monotonic, every row keeps its in-edge order and every column
+its out-edge order — results are bitwise those of one GPU.
+
+Per layer step the exchanges are:
+  forward : all-gather of the source-side projected rows (V | Q, el)
+  backward: all-gather of dO and the softmax records of the destination rows
+            (pass B needs them for every out-edge of the owned columns)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+def partition(n: int, row_ptr: torch.Tensor, csc_ptr: torch.Tensor, world: int) -> list[int]:
+    """Node boundaries b_0=0 <= ... <= b_world=n balancing in+out edges."""
+    cum = (row_ptr.to(torch.int64) + csc_ptr.to(torch.int64)).cpu()
+    total = int(cum[-1])
+    bounds = [0]
+    for k in range(1, world):
+        target = total * k // world
+        b = int(torch.searchsorted(cum, torch.tensor([target]), right=False)[0])
+        bounds.append(min(max(b, bounds[-1]), n))
+    bounds.append(n)
+    return bounds
+
+
+@dataclass
+class RowShard:
+    rank: int
+    world: int
+    n: int                 # original node count
+    bounds: list           # node boundaries, len world+1
+    R: int                 # padded rows per rank
+    row_ptr: torch.Tensor  # int32 [world*R + 1]: CSR of the owned rows (padded ids)
+    col: torch.Tensor      # int32 [e_csr]
+    csc_ptr: torch.Tensor  # int32 [world*R + 1]: CSC of the owned columns
+    csc_row: torch.Tensor  # int32 [e_csc]
+
+    @property
+    def n_padded(self) -> int:
+        return self.world * self.R
+
+    @property
+    def lo(self) -> int:
+        return self.bounds[self.rank]
+
+    @property
+    def hi(self) -> int:
+        return self.bounds[self.rank + 1]
+
+    @property
+    def rows(self) -> slice:
+        """This rank's block of a padded node table."""
+        return slice(self.rank * self.R, self.rank * self.R + (self.hi - self.lo))
+
+    @property
+    def block(self) -> slice:
+        return slice(self.rank * self.R, (self.rank + 1) * self.R)
+
+    # ------------------------------------------------------------ building --
+    @classmethod
+    def build(cls, n, row_ptr, col, csc_ptr, csc_row, rank, world) -> "RowShard":
+        """From the full canonical CSR/CSC (int64/int32 tensors on any device)."""
+        bounds = partition(n, row_ptr, csc_ptr, world)
+        R = max(1, max(bounds[k + 1] - bounds[k] for k in range(world)))
+        dev = col.device
+        b = torch.tensor(bounds, dtype=torch.int64, device=dev)
+
+        def relabel(ids):
+            ids = ids.to(torch.int64)
+            k = torch.searchsorted(b, ids, right=True) - 1
+            return (k * R + (ids - b[k])).to(torch.int32)
+
+        def side(ptr, idx):
+            lo, hi = bounds[rank], bounds[rank + 1]
+            p = ptr.to(torch.int64)
+            e0, e1 = int(p[lo]), int(p[hi])
+            out = torch.full((world * R + 1,), e1 - e0, dtype=torch.int64, device=dev)
+            out[: rank * R + 1] = 0
+            out[rank * R: rank * R + (hi - lo) + 1] = p[lo: hi + 1] - e0
+            return out.to(torch.int32), relabel(idx[e0:e1])
+
+        rp, c = side(row_ptr, col)
+        cp, cr = side(csc_ptr, csc_row)
+        return cls(rank, world, n, bounds, R, rp, c, cp, cr)
+
+    def to_padded(self, x: torch.Tensor) -> torch.Tensor:
+        """Full node table (original ids) -> padded table (world*R rows)."""
+        out = torch.zeros((self.n_padded,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        for k in range(self.world):
+            lo, hi = self.bounds[k], self.bounds[k + 1]
+            out[k * self.R: k * self.R + hi - lo] = x[lo:hi]
+        return out
+
+    def from_padded(self, xp: torch.Tensor) -> torch.Tensor:
+        parts = [xp[k * self.R: k * self.R + self.bounds[k + 1] - self.bounds[k]]
+                 for k in range(self.world)]
+        return torch.cat(parts, 0)
+
+    def device_graph(self, cta_threshold: int = 0, stream=None):
+        """gf_graph_t over the padded id space; empty (foreign) rows skipped."""
+        from .fused import DeviceGraph
+
+        return DeviceGraph.from_split(self.n_padded, self.row_ptr, self.col, self.csc_ptr,
+                                      self.csc_row, cta_threshold=cta_threshold, skip_empty=True,
+                                      stream=stream)
+
+
+def all_gather_rows(table: torch.Tensor, shard: RowShard, group=None, async_op=False):
+    """In-place all-gather of every rank's block of a padded node table."""
+    import torch.distributed as dist
+
+    blk = table[shard.block]
+    return dist.all_gather_into_tensor(table, blk, group=group, async_op=async_op)
