@@ -315,7 +315,7 @@ def run_reference(args, rank, world):
     out = {
         "metric": "fused AT-GNN layer fwd+bwd GEdges/s", "value": value, "unit": "GEdges/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "sample_edges": es, "sample": "1 head x row slice (1/16 of edges), x8 heads"},
         "cpu_baseline": {"value": value, "unit": "GEdges/s", "cores": os.cpu_count(),

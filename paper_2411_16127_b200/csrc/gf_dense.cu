@@ -8,11 +8,19 @@
 // bytes-bound time on C4 (233k x 64 x 64); the tcgen05 path is the planned
 // replacement for the ogbn-products GT shapes.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 
 namespace gfb {
+
+// gf_tc_gemm.cu
+bool tc_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, const void* A,
+                      const void* C);
+int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
+            int accumulate, cudaStream_t s);
+
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16;
@@ -211,6 +219,15 @@ extern "C" int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
+  // fp32 X*W: tcgen05 3xTF32 tensor-core kernel (gf_tc_gemm.cu).  GF_GEMM_SIMT=1
+  // forces the SIMT kernel (A/B measurements only).
+  static const bool force_simt = [] {
+    const char* e = std::getenv("GF_GEMM_SIMT");
+    return e && e[0] == '1';
+  }();
+  if (!force_simt && gfb::tc_gemm_eligible(dtype, trans_a, M, N, K, A, C))
+    return gfb::tc_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
+                        static_cast<float*>(C), accumulate, s);
   if (dtype == GF_F32)
     return gfb::gemm_impl<float>(trans_a, M, N, K, static_cast<const float*>(A),
                                  static_cast<const float*>(B), static_cast<float*>(C), accumulate, s);

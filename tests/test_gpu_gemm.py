@@ -1,0 +1,63 @@
+"""GPU: the dense projection (K0).  fp32 X·W runs on tcgen05 tensor cores with
+the 3xTF32 split; it must match an fp64 reference within the fp32 parity bar
+(floor-1 relative error <= 1e-5 here, 10x tighter than the 1e-4 layer bar;
+plain single-pass TF32 would be ~5e-4).  fp64 and X^T·dY use the SIMT kernel."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 32, 16), (1000, 64, 64), (333, 128, 384), (130, 36, 48),
+                                   (4097, 128, 256), (5, 8, 32)])
+def test_tc_gemm_3xtf32_matches_fp64(cuda, M, K, N):
+    from paper_2411_16127_b200 import fused
+
+    rng = np.random.default_rng(M + K + N)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    C = fused.gemm(torch.from_numpy(A).to(cuda), torch.from_numpy(B).to(cuda)).cpu().numpy()
+    assert rel_err(C, ref) < 1e-5, rel_err(C, ref)
+    # accumulate mode: C += A·B
+    Ct = torch.from_numpy(C).to(cuda)
+    fused.gemm(torch.from_numpy(A).to(cuda), torch.from_numpy(B).to(cuda), out=Ct, accumulate=True)
+    assert rel_err(Ct.cpu().numpy(), 2 * ref) < 1e-5
+
+
+def test_simt_paths(cuda):
+    from paper_2411_16127_b200 import fused
+
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (20000, 40))
+    dY = rng.uniform(-1, 1, (20000, 24))
+    for dt in (torch.float32, torch.float64):
+        out = fused.gemm(torch.tensor(X, dtype=dt, device=cuda), torch.tensor(dY, dtype=dt, device=cuda),
+                         trans_a=True).cpu().numpy()
+        assert rel_err(out, X.T @ dY) < (1e-4 if dt == torch.float32 else 1e-11)
+    W = rng.uniform(-1, 1, (40, 24))
+    out = fused.gemm(torch.tensor(X, device=cuda), torch.tensor(W, device=cuda)).cpu().numpy()
+    assert rel_err(out, X @ W) < 1e-11
+
+
+def test_gat_logits_and_fanin(cuda):
+    from paper_2411_16127_b200 import fused
+
+    rng = np.random.default_rng(4)
+    n, H, D = 777, 8, 8
+    Hf = rng.uniform(-1, 1, (n, H * D))
+    al, ar = rng.uniform(-1, 1, H * D), rng.uniform(-1, 1, H * D)
+    t = lambda a: torch.tensor(a, device=cuda)  # noqa: E731
+    el, er = fused.gat_logits(t(Hf), t(al), t(ar), H, D)
+    assert rel_err(el.cpu().numpy(), (Hf.reshape(n, H, D) * al.reshape(H, D)).sum(-1)) < 1e-12
+    assert rel_err(er.cpu().numpy(), (Hf.reshape(n, H, D) * ar.reshape(H, D)).sum(-1)) < 1e-12
+    dV = rng.uniform(-1, 1, (n, H * D))
+    dl, dr = rng.uniform(-1, 1, (n, H)), rng.uniform(-1, 1, (n, H))
+    dH, dal, dar = fused.gat_fanin(t(Hf), t(al), t(ar), t(dV), t(dl), t(dr), H, D)
+    ref = dV + (dl[:, :, None] * al.reshape(H, D) + dr[:, :, None] * ar.reshape(H, D)).reshape(n, -1)
+    assert rel_err(dH.cpu().numpy(), ref) < 1e-12
+    assert rel_err(dal.cpu().numpy(), (Hf.reshape(n, H, D) * dl[:, :, None]).sum(0).reshape(-1)) < 1e-11
+    assert rel_err(dar.cpu().numpy(), (Hf.reshape(n, H, D) * dr[:, :, None]).sum(0).reshape(-1)) < 1e-11
