@@ -269,6 +269,8 @@ def main():
     ap.add_argument("--cpu-frac", type=float, default=0.5,
                     help="edge fraction of the CPU-baseline row slice")
     ap.add_argument("--cta-threshold", type=int, default=0)
+    ap.add_argument("--no-layer", action="store_true",
+                    help="skip the layer-level (projection + pipeline) measurement")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args()
@@ -328,6 +330,76 @@ def run_reference(args, rank, world):
     }
     print(json.dumps(out))
     return 0
+
+
+def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush):
+    """Whole layer (projection + pipeline + weight grads) per step, fp32."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    lim = 1.0 / F ** 0.5
+    X = torch.rand(n, F, device=dev, generator=g) * 2 - 1
+    dO = torch.rand(n, F, device=dev, generator=g) * 2 - 1
+    rnd = lambda *s: (torch.rand(*s, device=dev, generator=g) * 2 - 1) * lim  # noqa: E731
+    gat = layer == "gat"
+    Wv = rnd(F, F)
+    if gat:
+        al, ar = rnd(F), rnd(F)
+    else:
+        Wq, Wk = rnd(F, F), rnd(F, F)
+    Hf = torch.empty(n, F, device=dev)
+    Qb = torch.empty(n, F, device=dev)
+    Kb = torch.empty(n, F, device=dev)
+    O = torch.empty(n, F, device=dev)
+    st = torch.empty(n, H, 4, device=dev)
+    qk = spec.qk_width
+    dQ, dK, dV = (torch.empty(n, qk, device=dev), torch.empty(n, qk, device=dev),
+                  torch.empty(n, F, device=dev))
+    dW = [torch.empty(F, F, device=dev) for _ in range(3)]
+
+    def step(ev=None):
+        rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
+        rec(0)
+        if gat:
+            fused.gemm(X, Wv, out=Hf, stream=stream)
+            el, er = fused.gat_logits(Hf, al, ar, H, D, stream=stream)
+            q, k, v = el, er, Hf
+        else:
+            fused.gemm(X, Wq, out=Qb, stream=stream)
+            fused.gemm(X, Wk, out=Kb, stream=stream)
+            fused.gemm(X, Wv, out=Hf, stream=stream)
+            q, k, v = Qb, Kb, Hf
+        rec(1)
+        fused.attn_forward(dg, spec, q, k, v, O=O, stats=st, stream=stream)
+        fused.attn_backward_rows(dg, spec, q, k, v, O, st, dO, dK, stream=stream)
+        fused.attn_backward_cols(dg, spec, q, k, v, st, dO, dQ, dV, stream=stream)
+        rec(2)
+        if gat:
+            dH, dal, dar = fused.gat_fanin(Hf, al, ar, dV, dQ, dK, H, D, stream=stream)
+            fused.gemm(X, dH, trans_a=True, out=dW[0], stream=stream)
+        else:
+            for w_, d_ in zip(dW, (dQ, dK, dV)):
+                fused.gemm(X, d_, trans_a=True, out=w_, stream=stream)
+        rec(3)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = max(5, args.steps // 5)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for i in range(K):
+        flush.zero_()
+        step(evs[i])
+    torch.cuda.synchronize()
+    seg = lambda j: sum(a[j].elapsed_time(a[j + 1]) for a in evs) / K  # noqa: E731
+    ms = sum(a[0].elapsed_time(a[3]) for a in evs) / K
+    return {"value": e / (ms / 1e3) / 1e9, "unit": "GEdges/s", "ms_per_step": ms,
+            "projection_fwd_ms": seg(0), "pipeline_ms": seg(1), "weight_grad_ms": seg(2),
+            "projection": "X*W on tcgen05 (3xTF32, UTCHMMA); X^T*dY SIMT split-K",
+            "x_width": F}
 
 
 def run_ours(args, rank, world):
@@ -453,12 +525,40 @@ def run_ours(args, rank, world):
         h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hdO))
         d2h = sum(x.numel() * x.element_size() for x in (hO, hdQ, hdK, hdV))
 
+        # Copies overlap compute WITHIN the step (each step still moves all of
+        # its own inputs H2D and outputs D2H): dO's H2D runs under the forward,
+        # O's D2H under the backward, dK's D2H under pass B.
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
         def e2e_step():
-            for h, d in ((hQ, Q), (hK, K), (hV, V), (hdO, dO)):
+            ev_start = torch.cuda.Event()
+            ev_start.record(stream)
+            for h, d in ((hQ, Q), (hK, K), (hV, V)):
                 d.copy_(h, non_blocking=True)
-            step()
-            for h, d in ((hO, O), (hdQ, dQ), (hdK, dK), (hdV, dV)):
+            s_in.wait_event(ev_start)
+            with torch.cuda.stream(s_in):
+                dO.copy_(hdO, non_blocking=True)
+            ev_do = torch.cuda.Event()
+            ev_do.record(s_in)
+            fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream)
+            ev_f = torch.cuda.Event()
+            ev_f.record(stream)
+            s_out.wait_event(ev_f)
+            with torch.cuda.stream(s_out):
+                hO.copy_(O, non_blocking=True)
+            stream.wait_event(ev_do)
+            fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK, stream=stream)
+            ev_a = torch.cuda.Event()
+            ev_a.record(stream)
+            s_out.wait_event(ev_a)
+            with torch.cuda.stream(s_out):
+                hdK.copy_(dK, non_blocking=True)
+            fused.attn_backward_cols(dg, spec, Q, K, V, stats, dO, dQ, dV, stream=stream)
+            for h, d in ((hdQ, dQ), (hdV, dV)):
                 h.copy_(d, non_blocking=True)
+            ev_o = torch.cuda.Event()
+            ev_o.record(s_out)
+            stream.wait_event(ev_o)
 
         for _ in range(2):
             e2e_step()
@@ -473,6 +573,14 @@ def run_ours(args, rank, world):
             b.synchronize()
             ee.append(a.elapsed_time(b))
         e2e_val = e / (statistics.mean(ee) / 1e3) / 1e9
+
+    # ---- layer level (projections reported separately): the
+    # conv_forward / conv_backward step of models.hpp:104-158 with X of width
+    # F (bench.cpp:86-87): X·W on tcgen05 (3xTF32), GAT logits / fan-in,
+    # the fused pipeline, and the weight gradients X^T·dH.
+    layer_out = None
+    if not sharded and not args.no_layer:
+        layer_out = layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush)
 
     # ---- roofline of the dominant kernel
     means = {"fwd": statistics.mean(k_fwd), "bwd_rows": statistics.mean(k_ra),
@@ -529,6 +637,7 @@ def run_ours(args, rank, world):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "GEdges/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
+            "layer": layer_out,
             "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
         }
