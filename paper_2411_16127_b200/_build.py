@@ -81,6 +81,12 @@ def build(verbose: bool = False) -> None:
     if _newer(HOST_LIB, host_obj + [CUDA_LIB]):
         _run([CXX, "-shared", "-o", HOST_LIB] + host_obj
              + [f"-L{PKG}", "-lgraphfuse_cuda", "-Wl,-rpath,$ORIGIN"])
+    # C++ drop-in test binary: reference-style C++ code against include/graphfuse
+    test_src = os.path.join(ROOT, "tests", "cpp", "dropin_tests.cpp")
+    test_bin = os.path.join(ROOT, "tests", "cpp", "dropin_tests")
+    if os.path.exists(test_src) and _newer(test_bin, [test_src, HOST_LIB] + hdrs):
+        _run([CXX] + CXX_FLAGS + [test_src, "-o", test_bin, f"-L{PKG}", "-lgraphfuse",
+                                  "-lgraphfuse_cuda", f"-Wl,-rpath,{PKG}"])
     bind = os.path.join(CSRC, "host", "gf_host_bindings.cpp")
     if _newer(CORE, [bind, HOST_LIB] + hdrs):
         import pybind11

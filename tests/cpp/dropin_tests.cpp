@@ -1,0 +1,233 @@
+// C++ drop-in check: code written against the reference's operator API
+// (#include "graphfuse/engine.hpp" etc., namespace graphfuse, templates on T)
+// compiles unchanged against include/graphfuse and runs on the B200 path via
+// libgraphfuse.so -> libgraphfuse_cuda.so.  The cases restate the reference's
+// own unit tests (test_engine.cpp, test_autograd.cpp, test_models.cpp) with
+// this file's own harness.  Exit code 0 = all checks passed.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "graphfuse/autograd.hpp"
+#include "graphfuse/engine.hpp"
+#include "graphfuse/models.hpp"
+
+using namespace graphfuse;
+
+static int g_checks = 0, g_fail = 0;
+#define EXPECT(cond)                                                             \
+  do {                                                                           \
+    ++g_checks;                                                                  \
+    if (!(cond)) {                                                               \
+      ++g_fail;                                                                  \
+      std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);                \
+    }                                                                            \
+  } while (0)
+
+template <typename T>
+static double floor1(const DenseMatrix<T>& a, const DenseMatrix<T>& b) {
+  double w = 0;
+  for (size_t i = 0; i < a.data.size(); ++i) {
+    const double x = a.data[i], y = b.data[i];
+    w = std::max(w, std::abs(x - y) / std::max({std::abs(x), std::abs(y), 1.0}));
+  }
+  return w;
+}
+
+// Dense masked reference of the single-head forward (independent of the API).
+template <typename T>
+static DenseMatrix<T> dense_forward(const Graph& g, const PipelineInputs<T>& in) {
+  const auto& k = in.kind;
+  DenseMatrix<T> O(g.num_nodes, in.V.cols);
+  auto norm_rows = [](const DenseMatrix<T>& X) {
+    DenseMatrix<T> Y = X;
+    for (std::int64_t r = 0; r < X.rows; ++r) {
+      double s = 0;
+      for (std::int64_t c = 0; c < X.cols; ++c) s += double(X.at(r, c)) * X.at(r, c);
+      const double n = std::max(std::sqrt(s), 1e-12);
+      for (std::int64_t c = 0; c < X.cols; ++c) Y.at(r, c) = T(X.at(r, c) / n);
+    }
+    return Y;
+  };
+  const DenseMatrix<T> Q = k.l2_normalize_inputs ? norm_rows(in.Q) : in.Q;
+  const DenseMatrix<T> K = k.l2_normalize_inputs ? norm_rows(in.K) : in.K;
+  for (NodeId v = 0; v < g.num_nodes; ++v) {
+    const EdgeId b = g.csr_row_ptr[v], e = g.csr_row_ptr[v + 1];
+    if (b == e) continue;
+    std::vector<double> s;
+    for (EdgeId i = b; i < e; ++i) {
+      const NodeId u = g.csr_col_idx[i];
+      if (k.variant == SddmmVariant::Dot) {
+        double d = 0;
+        for (std::int64_t c = 0; c < Q.cols; ++c) d += double(Q.at(u, c)) * K.at(v, c);
+        s.push_back(k.scale * d);
+      } else {
+        const double x = double(Q.data[u]) + K.data[v];
+        s.push_back(x >= 0 ? x : k.leaky_slope * x);
+      }
+    }
+    double m = s[0], z = 0;
+    for (double x : s) m = std::max(m, x);
+    for (double& x : s) z += (x = std::exp(x - m));
+    for (std::int64_t c = 0; c < in.V.cols; ++c) {
+      double acc = 0;
+      for (EdgeId i = b; i < e; ++i) acc += s[i - b] / z * in.V.at(g.csr_col_idx[i], c);
+      O.at(v, c) = T(acc);
+    }
+  }
+  return O;
+}
+
+static void modes_match_dense() {
+  for (std::uint64_t seed = 0; seed < 6; ++seed) {
+    Graph g = gen_random(48 + seed * 30, 6, seed);
+    ConvSpec spec;
+    spec.model = seed % 3 == 0 ? Model::GT : seed % 3 == 1 ? Model::AGNN : Model::GAT;
+    spec.dim = 8;
+    auto in = make_pipeline_inputs<float>(g, spec, seed + 100);
+    const auto ref = dense_forward(g, in);
+    FusionPlan plan;
+    for (Strategy m : {Strategy::Unfused, Strategy::Smmf, Strategy::Pmf,
+                       Strategy::FeatureParallelBaseline}) {
+      auto res = run_strategy(g, in.Q, in.K, in.V, in.kind, plan.with_strategy(m));
+      EXPECT(floor1(res.O, ref) < 2e-5);
+      EXPECT(res.ctx.P.size() == g.num_edges);
+      for (NodeId v = 0; v < g.num_nodes; ++v) {
+        double sum = 0;
+        for (EdgeId i = g.csr_row_ptr[v]; i < g.csr_row_ptr[v + 1]; ++i) sum += res.ctx.P[i];
+        if (g.in_degree(v) > 0) EXPECT(std::abs(sum - 1.0) < 1e-5);
+      }
+    }
+  }
+}
+
+static void launches_and_traffic() {
+  Graph g = gen_random(1000, 10, 5);
+  EXPECT(g.num_edges == 10000);
+  auto V = random_matrix<float>(1000, 4, 1), Q = random_matrix<float>(1000, 4, 2),
+       K = random_matrix<float>(1000, 4, 3);
+  FusionPlan plan;
+  EXPECT(run_unfused(g, Q, K, V, SddmmKind::dot()).counters.kernel_launches == 3);
+  EXPECT(run_pmf(g, Q, K, V, SddmmKind::dot(), plan).counters.kernel_launches == 2);
+  EXPECT(run_smmf(g, Q, K, V, SddmmKind::dot(), plan).counters.kernel_launches == 1);
+  const std::uint64_t eb = 10000 * 4;
+  auto un = run_unfused(g, Q, K, V, SddmmKind::dot(), plan).counters;
+  auto sm = run_smmf(g, Q, K, V, SddmmKind::dot(), plan).counters;
+  EXPECT(un.s_global_bytes == 2 * eb && un.f_global_bytes == 2 * eb && un.p_global_bytes == 2 * eb);
+  EXPECT(sm.s_global_bytes == 0 && sm.p_global_bytes == eb);
+}
+
+static void feasibility_error() {
+  Graph g = gen_super_node(100, 2, 90, 1);
+  auto V = random_matrix<float>(100, 8, 1);
+  FusionPlan plan;
+  plan.shared_mem_budget_bytes = 256;
+  bool threw = false;
+  try {
+    run_smmf(g, V, V, V, SddmmKind::dot(), plan);
+  } catch (const EngineError& e) {
+    const std::string msg = e.what();
+    threw = msg.find("block 0") != std::string::npos && msg.find("requires") != std::string::npos;
+  }
+  EXPECT(threw);
+}
+
+static void backward_cases() {
+  // fused == unfused values, launches 3/5 (test_autograd.cpp "fused backward equals ...")
+  for (std::uint64_t seed = 0; seed < 6; ++seed) {
+    Graph g = gen_random(20 + seed * 40, 5, seed);
+    ConvSpec spec;
+    spec.model = seed % 3 == 0 ? Model::GT : seed % 3 == 1 ? Model::AGNN : Model::GAT;
+    spec.dim = 5;
+    auto in = make_pipeline_inputs<double>(g, spec, seed + 50);
+    ForwardContext<double> ctx;
+    ctx.g = &g;
+    ctx.Q = in.Q;
+    ctx.K = in.K;
+    ctx.V = in.V;
+    ctx.kind = in.kind;
+    auto dO = random_matrix<double>(g.num_nodes, 5, seed + 60);
+    auto f = fused_backward(g, ctx, dO, FusionPlan{});
+    auto u = unfused_backward(g, ctx, dO);
+    EXPECT(f.counters.kernel_launches == 3 && u.counters.kernel_launches == 5);
+    EXPECT(!f.counters.fallback_unfused);
+    EXPECT(floor1(f.grads.dQ, u.grads.dQ) < 1e-12 && floor1(f.grads.dV, u.grads.dV) < 1e-12);
+  }
+  // linearity in dO and zero dO (test_autograd.cpp)
+  Graph g = gen_random(30, 4, 11);
+  ConvSpec spec;
+  spec.model = Model::GT;
+  spec.dim = 3;
+  auto in = make_pipeline_inputs<double>(g, spec, 12);
+  auto res = run_strategy(g, in.Q, in.K, in.V, in.kind, FusionPlan{});
+  auto dO = random_matrix<double>(30, 3, 13);
+  auto one = unfused_backward(g, res.ctx, dO);
+  for (double& v : dO.data) v *= -2.5;
+  auto two = unfused_backward(g, res.ctx, dO);
+  for (size_t i = 0; i < one.grads.dV.data.size(); ++i)
+    EXPECT(std::abs(two.grads.dV.data[i] + 2.5 * one.grads.dV.data[i]) < 1e-10);
+  auto zero = fused_backward(g, res.ctx, DenseMatrix<double>(30, 3), FusionPlan{});
+  for (double v : zero.grads.dQ.data) EXPECT(v == 0.0);
+  // finite differences (autograd.hpp:241-287) for all three models
+  for (Model m : {Model::GT, Model::AGNN, Model::GAT}) {
+    Graph gg = gen_random(12, 4, 21 + static_cast<int>(m));
+    ConvSpec s;
+    s.model = m;
+    s.dim = 4;
+    auto pin = make_pipeline_inputs<double>(gg, s, 22);
+    EXPECT(finite_difference_check(gg, pin.Q, pin.K, pin.V, pin.kind, 1e-5) < 1e-6);
+  }
+}
+
+static void layer_cases() {
+  // GT with identity weights reduces to the raw pipeline (test_models.cpp)
+  Graph g = gen_random(40, 4, 1);
+  ConvSpec spec;
+  spec.model = Model::GT;
+  spec.dim = 8;
+  auto X = random_matrix<double>(40, 8, 2);
+  ConvWeights<double> w;
+  w.W_q = w.W_k = w.W_v = DenseMatrix<double>(8, 8);
+  for (int i = 0; i < 8; ++i) w.W_q.at(i, i) = w.W_k.at(i, i) = w.W_v.at(i, i) = 1;
+  auto [O, ctx] = conv_forward(spec, g, X, w);
+  FusionPlan plan;
+  plan.strategy = ctx.fwd.plan.strategy;
+  auto ref = run_strategy(g, X, X, X, kind_for(spec), plan);
+  EXPECT(floor1(O, ref.O) < 1e-14);
+  EXPECT(std::abs(ctx.fwd.kind.scale - 1.0 / std::sqrt(8.0)) < 1e-15);
+  // conv_backward vs finite differences on W_v (GAT)
+  ConvSpec gs;
+  gs.model = Model::GAT;
+  gs.dim = 3;
+  auto Xg = random_matrix<double>(40, 4, 9);
+  auto wg = random_weights<double>(gs, 4, 12);
+  auto fw = conv_forward(gs, g, Xg, wg);
+  auto grads = conv_backward(gs, g, fw.second, wg, DenseMatrix<double>(40, 3, 1.0));
+  auto loss = [&](ConvWeights<double>& ww) {
+    auto out = conv_forward(gs, g, Xg, ww).first;
+    double s = 0;
+    for (double v : out.data) s += v;
+    return s;
+  };
+  for (size_t i = 0; i < wg.W_v.data.size(); i += 2) {
+    const double keep = wg.W_v.data[i], h = 1e-6;
+    wg.W_v.data[i] = keep + h;
+    const double up = loss(wg);
+    wg.W_v.data[i] = keep - h;
+    const double dn = loss(wg);
+    wg.W_v.data[i] = keep;
+    const double fd = (up - dn) / (2 * h), a = grads.dW_v.data[i];
+    EXPECT(std::abs(fd - a) / std::max({std::abs(fd), std::abs(a), 1.0}) < 1e-6);
+  }
+}
+
+int main() {
+  modes_match_dense();
+  launches_and_traffic();
+  feasibility_error();
+  backward_cases();
+  layer_cases();
+  std::printf("%d checks, %d failed\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
