@@ -3,10 +3,9 @@
 // logits el/er and the GAT fan-in.  All deterministic (fixed reduction
 // orders, split-K partials reduced in order; no atomics).
 //
-// gf_gemm is a register-tiled FP32/FP64 SIMT GEMM (64x64 tile, 4x4 per
-// thread).  At the BASELINE shapes the projection is <2% of the layer's
-// bytes-bound time on C4 (233k x 64 x 64); the tcgen05 path is the planned
-// replacement for the ogbn-products GT shapes.
+// gf_gemm dispatches fp32 X·W and X^T·dY to the tcgen05 3xTF32 tensor-core
+// kernels (gf_tc_gemm.cu); fp64 and other shapes use the register-tiled SIMT
+// GEMM below (64x64 tile, 4x4 per thread, deterministic split-K).
 #include <algorithm>
 #include <cstdlib>
 
@@ -20,6 +19,10 @@ bool tc_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, c
                       const void* C);
 int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
             int accumulate, cudaStream_t s);
+bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                         const void* B);
+int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
+               int accumulate, cudaStream_t s);
 
 namespace {
 
@@ -228,6 +231,9 @@ extern "C" int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int
   if (!force_simt && gfb::tc_gemm_eligible(dtype, trans_a, M, N, K, A, C))
     return gfb::tc_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
                         static_cast<float*>(C), accumulate, s);
+  if (!force_simt && trans_a && gfb::tc_gemm_tn_eligible(dtype, M, N, K, A, B))
+    return gfb::tc_gemm_tn(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
+                           static_cast<float*>(C), accumulate, s);
   if (dtype == GF_F32)
     return gfb::gemm_impl<float>(trans_a, M, N, K, static_cast<const float*>(A),
                                  static_cast<const float*>(B), static_cast<float*>(C), accumulate, s);

@@ -17,6 +17,7 @@
 // thread = row) and writes C.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "gf_internal.cuh"
@@ -210,7 +211,174 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
 }
 
+// ---------------------------------------------------------------------------
+// Weight gradients C[M x N] = A^T·B with A = X (K x M) and B = dY (K x N), both
+// row-major, K = number of nodes (millions), M = F_in, N = F_out (<= 256).
+// Both operands are MN-major for the MMA (A[m][k] = X[k][m], contiguous in m).
+// Deterministic split-K: CTA z owns K rows [z*Ks, (z+1)*Ks) and writes its
+// M x N partial; a fixed-order reduction sums the partials.
+// MN-major no-swizzle canonical layout (cute: ((T,1,m),(8,k)):((1,T,SBO),(1T,LBO))):
+// core matrix = 8 K-rows x 16 B (4 MN elements) = 128 contiguous bytes;
+// core (kg, mg) at (kg*MG + mg)*128 => SBO = 128 (next MN group), LBO = MG*128
+// (next K group); one tf32 MMA (K = 8) consumes one K group.
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_tn_3xtf32(int M, int N, int K, int ks, const float* __restrict__ A,
+                      const float* __restrict__ B, float* __restrict__ part) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int NP = N;                 // multiple of 16 (UMMA N)
+  const int MG = TC_M / 4, NG = NP / 4;
+  float* a_hi = reinterpret_cast<float*>(smem);
+  float* a_lo = a_hi + TC_M * TC_KC;
+  float* b_hi = a_lo + TC_M * TC_KC;
+  float* b_lo = b_hi + NP * TC_KC;
+  const uint32_t ncols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  // D f32, A/B tf32, A MN-major (bit 15), B MN-major (bit 16)
+  const uint32_t idesc = instr_desc_tf32(TC_M, NP) | (1u << 15) | (1u << 16);
+  const uint32_t lbo_a = MG * 128, lbo_b = NG * 128, sbo = 128;
+  const int kb = blockIdx.x * ks, ke = min(K, kb + ks);
+  uint32_t phase = 0;
+  bool first = true;
+  for (int k0 = kb; k0 < ke; k0 += TC_KC) {
+    // lane = K row of the chunk; the warp's MN groups are a quarter of the tile
+    const int kl = lane, k = k0 + kl;
+    const bool kin = k < ke;
+    const int coff = ((kl / 8) * 0 + (kl % 8)) * 4;  // float offset of the K row in a core
+    for (int mg = warp; mg < MG; mg += 4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kin && mg * 4 < M) v = *reinterpret_cast<const float4*>(A + static_cast<size_t>(k) * M + mg * 4);
+      float4 h, l;
+      split_tf32(v.x, h.x, l.x);
+      split_tf32(v.y, h.y, l.y);
+      split_tf32(v.z, h.z, l.z);
+      split_tf32(v.w, h.w, l.w);
+      const int off = ((kl / 8) * MG + mg) * 32 + coff;
+      *reinterpret_cast<float4*>(a_hi + off) = h;
+      *reinterpret_cast<float4*>(a_lo + off) = l;
+    }
+    for (int ng = warp; ng < NG; ng += 4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kin) v = *reinterpret_cast<const float4*>(B + static_cast<size_t>(k) * N + ng * 4);
+      float4 h, l;
+      split_tf32(v.x, h.x, l.x);
+      split_tf32(v.y, h.y, l.y);
+      split_tf32(v.z, h.z, l.z);
+      split_tf32(v.w, h.w, l.w);
+      const int off = ((kl / 8) * NG + ng) * 32 + coff;
+      *reinterpret_cast<float4*>(b_hi + off) = h;
+      *reinterpret_cast<float4*>(b_lo + off) = l;
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi),
+                     bl = smem_u32(b_lo);
+#pragma unroll
+      for (int s = 0; s < TC_KC / 8; ++s) {
+        const uint64_t dah = smem_desc(ah + s * lbo_a, lbo_a, sbo), dal = smem_desc(al + s * lbo_a, lbo_a, sbo);
+        const uint64_t dbh = smem_desc(bh + s * lbo_b, lbo_b, sbo), dbl = smem_desc(bl + s * lbo_b, lbo_b, sbo);
+        mma_tf32(tmem, dah, dbh, idesc, (!first || s > 0) ? 1u : 0u);
+        mma_tf32(tmem, dah, dbl, idesc, 1u);
+        mma_tf32(tmem, dal, dbh, idesc, 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&mbar)));
+    }
+    mbar_wait(smem_u32(&mbar), phase);
+    phase ^= 1;
+    first = false;
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = t;  // TMEM lane = output row m
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  float* dst = part + static_cast<size_t>(blockIdx.x) * M * N + static_cast<size_t>(row) * N;
+  for (int c = 0; c < NP; c += 16) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(tmem + lane_base + c));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (row < M && !first) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(dst + c + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    } else if (row < M) {  // empty K slice
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+}
+
+__global__ void tn_reduce(const float* __restrict__ part, int splits, size_t mn,
+                          float* __restrict__ C, int accumulate) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < mn;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[z * mn + i];  // fixed order: deterministic
+    C[i] = accumulate ? C[i] + s : s;
+  }
+}
+
 }  // namespace
+
+bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                         const void* B) {
+  if (dtype != GF_F32 || M <= 0 || M > TC_M || M % 4 || N <= 0 || N > 256 || N % 16 ||
+      K <= 0)
+    return false;
+  return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0;
+}
+
+int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
+               int accumulate, cudaStream_t s) {
+  const int64_t target = std::min<int64_t>(296, (K + 1023) / 1024);
+  int64_t ks = (K + target - 1) / target;
+  ks = ((ks + TC_KC - 1) / TC_KC) * TC_KC;
+  const int splits = static_cast<int>((K + ks - 1) / ks);
+  float* part = nullptr;
+  GF_CHECK_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * M * N, s));
+  const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC);
+  GF_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_tn_3xtf32,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+  tc_gemm_tn_3xtf32<<<splits, TC_THREADS, smem, s>>>(static_cast<int>(M), static_cast<int>(N),
+                                                     static_cast<int>(K), static_cast<int>(ks), A,
+                                                     B, part);
+  GF_CHECK_LAUNCH("tc_gemm_tn_3xtf32");
+  const size_t mn = static_cast<size_t>(M) * N;
+  tn_reduce<<<static_cast<int>(std::min<size_t>(1024, (mn + 255) / 256)), 256, 0, s>>>(
+      part, splits, mn, C, accumulate);
+  GF_CHECK_LAUNCH("tn_reduce");
+  cudaFreeAsync(part, s);
+  return GF_OK;
+}
 
 // Tensor-core eligibility: fp32, C = A·B (not transposed), N a multiple of 16,
 // 16-byte aligned rows.  N is tiled by the largest multiple of 16 <= 256 that

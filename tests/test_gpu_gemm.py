@@ -28,6 +28,24 @@ def test_tc_gemm_3xtf32_matches_fp64(cuda, M, K, N):
     assert rel_err(Ct.cpu().numpy(), 2 * ref) < 5e-5
 
 
+@pytest.mark.parametrize("K,M,N", [(50_000, 64, 64), (100_000, 128, 128), (1000, 128, 256),
+                                   (33, 8, 16), (700_001, 128, 64)])
+def test_tc_weight_grad_xt_dy(cuda, K, M, N):
+    """dW = X^T dY on tcgen05 (MN-major operands, deterministic split-K)."""
+    from paper_2411_16127_b200 import fused
+
+    rng = np.random.default_rng(K + M + N)
+    X = rng.uniform(-1, 1, (K, M)).astype(np.float32)
+    dY = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    ref = X.T.astype(np.float64) @ dY.astype(np.float64)
+    tx, ty = torch.from_numpy(X).to(cuda), torch.from_numpy(dY).to(cuda)
+    C = fused.gemm(tx, ty, trans_a=True)
+    C2 = fused.gemm(tx, ty, trans_a=True)
+    scale = max(1.0, float(np.abs(ref).max()))
+    assert float(np.abs(C.cpu().numpy() - ref).max()) / scale < 5e-5
+    assert torch.equal(C, C2)  # fixed-order split-K reduction
+
+
 def test_simt_paths(cuda):
     from paper_2411_16127_b200 import fused
 
