@@ -254,8 +254,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t lbo_a = MG * 128, lbo_b = NG * 128, sbo = 128;
   const int kb = blockIdx.x * ks, ke = min(K, kb + ks);
   uint32_t phase = 0;
-  bool first = true;
+  // fp32 round-to-nearest accumulator in smem (row stride NP + 4: conflict-free
+  // float4 rows); TMEM accumulates at most kSub K rows before it is drained
+  // here, bounding the tensor core's truncating accumulation error.
+  constexpr int kSub = 1024;
+  float* acc_s = b_lo + NP * TC_KC;
+  const int AS = NP + 4;
+  for (int i = t; i < TC_M * AS; i += TC_THREADS) acc_s[i] = 0.f;
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  int sub0 = kb;
   for (int k0 = kb; k0 < ke; k0 += TC_KC) {
+    if (k0 - sub0 >= kSub) sub0 = k0;
     // lane = K row of the chunk; the warp's MN groups are a quarter of the tile
     const int kl = lane, k = k0 + kl;
     const bool kin = k < ke;
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int s = 0; s < TC_KC / 8; ++s) {
         const uint64_t dah = smem_desc(ah + s * lbo_a, lbo_a, sbo), dal = smem_desc(al + s * lbo_a, lbo_a, sbo);
         const uint64_t dbh = smem_desc(bh + s * lbo_b, lbo_b, sbo), dbl = smem_desc(bl + s * lbo_b, lbo_b, sbo);
-        mma_tf32(tmem, dah, dbh, idesc, (!first || s > 0) ? 1u : 0u);
+        mma_tf32(tmem, dah, dbh, idesc, (k0 > sub0 || s > 0) ? 1u : 0u);
         mma_tf32(tmem, dah, dbl, idesc, 1u);
         mma_tf32(tmem, dal, dbh, idesc, 1u);
       }
@@ -303,31 +312,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     mbar_wait(smem_u32(&mbar), phase);
     phase ^= 1;
-    first = false;
+    const int nk = k0 + TC_KC;
+    if (nk >= ke || nk - sub0 >= kSub) {  // drain this sub-slice: TMEM -> smem (RN adds)
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int c = 0; c < NP; c += 16) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+              "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+              "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(tmem + lane_base + c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        float* a = acc_s + t * AS + c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();  // TMEM reads complete before the next sub-slice's MMAs
+    }
   }
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = t;  // TMEM lane = output row m
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  const int row = t;
   float* dst = part + static_cast<size_t>(blockIdx.x) * M * N + static_cast<size_t>(row) * N;
   for (int c = 0; c < NP; c += 16) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(tmem + lane_base + c));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (row < M && !first) {
+    if (row < M) {
 #pragma unroll
       for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(dst + c + j) =
-            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-    } else if (row < M) {  // empty K slice
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(dst + c + j) = *reinterpret_cast<const float4*>(acc_s + t * AS + c + j);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -364,7 +376,8 @@ int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, 
   const int splits = static_cast<int>((K + ks - 1) / ks);
   float* part = nullptr;
   GF_CHECK_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * M * N, s));
-  const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC);
+  const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC +
+                                      TC_M * static_cast<size_t>(N + 4));
   GF_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_tn_3xtf32,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));

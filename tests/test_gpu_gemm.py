@@ -42,7 +42,8 @@ def test_tc_weight_grad_xt_dy(cuda, K, M, N):
     C = fused.gemm(tx, ty, trans_a=True)
     C2 = fused.gemm(tx, ty, trans_a=True)
     scale = max(1.0, float(np.abs(ref).max()))
-    assert float(np.abs(C.cpu().numpy() - ref).max()) / scale < 5e-5
+    err = float(np.abs(C.cpu().numpy() - ref).max()) / scale
+    assert err < 5e-5, err
     assert torch.equal(C, C2)  # fixed-order split-K reduction
 
 
