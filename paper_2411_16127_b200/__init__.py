@@ -39,7 +39,7 @@ try:
 except ImportError as _e:  # fail loudly: there is no pure-Python / CPU fallback
     raise ImportError(
         f"paper_2411_16127_b200: compiled extension missing or broken ({_e}); run "
-        "`python -c 'import paper_2411_16127_b200._build as b; b.build()'`") from _e
+        "`python paper_2411_16127_b200/_build.py` (or __graft_entry__.build())") from _e
 
 __all__ = [
     "Graph",
