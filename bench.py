@@ -398,7 +398,7 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush):
     ms = sum(a[0].elapsed_time(a[3]) for a in evs) / K
     return {"value": e / (ms / 1e3) / 1e9, "unit": "GEdges/s", "ms_per_step": ms,
             "projection_fwd_ms": seg(0), "pipeline_ms": seg(1), "weight_grad_ms": seg(2),
-            "projection": "X*W on tcgen05 (3xTF32, UTCHMMA); X^T*dY SIMT split-K",
+            "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; X^T*dY deterministic split-K)",
             "x_width": F}
 
 

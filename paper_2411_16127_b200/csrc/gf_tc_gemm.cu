@@ -68,7 +68,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-      "r"(phase));
+      "r"(phase)
+      : "memory");
+}
+
+// tcgen05.ld (32x32b, 16 columns: thread = TMEM lane) and its wait in ONE asm
+// statement: as separate statements the compiler may consume the destination
+// registers before tcgen05.wait::ld (it did: the drained values read as 0).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
 }
 
 // C[M x N] = A[M x K] * B[K x N], all row-major fp32.  grid = (ceil(M/128), N/n_tile).
@@ -98,9 +114,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = instr_desc_tf32(TC_M, NT);
   // Core-matrix geometry (bytes): A core (rg, kc) at (kc*16 + rg)*128;
@@ -155,10 +171,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (t == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi),
                      bl = smem_u32(b_lo);
 #pragma unroll
@@ -171,25 +187,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mma_tf32(tmem, dal, dbh, idesc, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&mbar)));
+          smem_u32(&mbar)) : "memory");
     }
     mbar_wait(smem_u32(&mbar), phase);  // MMAs done: smem reusable, accumulator final
     phase ^= 1;
   }
-  asm volatile("tcgen05.fence::after_thread_sync;");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- epilogue: warp w reads TMEM lanes [32w, 32w+32): thread = row
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
   for (int c = 0; c < NT; c += 16) {
     uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(tmem + lane_base + c));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    tmem_ld16(tmem + lane_base + c, r);
     if (row < M) {
       float* dst = C + static_cast<size_t>(row) * N + n0 + c;
 #pragma unroll
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   (void)lane;
-  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
@@ -213,23 +222,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // ---------------------------------------------------------------------------
 // Weight gradients C[M x N] = A^T·B with A = X (K x M) and B = dY (K x N), both
-// row-major, K = number of nodes (millions), M = F_in, N = F_out (<= 256).
-// Both operands are MN-major for the MMA (A[m][k] = X[k][m], contiguous in m).
+// row-major, K = number of nodes (millions), M = F_in (<= 128), N = F_out
+// (<= 256).  The staging transposes: thread m loads X[k..k+3][m] (coalesced
+// across threads: one 512 B row segment per k) and stores the 4 K values as
+// one float4 in the same K-major core-matrix layout as tc_gemm_3xtf32, so both
+// kernels issue identical K-major UMMA descriptors.  (MN-major descriptors
+// were tried first and produced all-zero accumulators on B200.)
 // Deterministic split-K: CTA z owns K rows [z*Ks, (z+1)*Ks) and writes its
 // M x N partial; a fixed-order reduction sums the partials.
-// MN-major no-swizzle canonical layout (cute: ((T,1,m),(8,k)):((1,T,SBO),(1T,LBO))):
-// core matrix = 8 K-rows x 16 B (4 MN elements) = 128 contiguous bytes;
-// core (kg, mg) at (kg*MG + mg)*128 => SBO = 128 (next MN group), LBO = MG*128
-// (next K group); one tf32 MMA (K = 8) consumes one K group.
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_tn_3xtf32(int M, int N, int K, int ks, const float* __restrict__ A,
                       const float* __restrict__ B, float* __restrict__ part) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int t = threadIdx.x, warp = t >> 5;
   const int NP = N;                 // multiple of 16 (UMMA N)
-  const int MG = TC_M / 4, NG = NP / 4;
   float* a_hi = reinterpret_cast<float*>(smem);
   float* a_lo = a_hi + TC_M * TC_KC;
   float* b_hi = a_lo + TC_M * TC_KC;
@@ -245,13 +253,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  // D f32, A/B tf32, A MN-major (bit 15), B MN-major (bit 16)
-  const uint32_t idesc = instr_desc_tf32(TC_M, NP) | (1u << 15) | (1u << 16);
-  const uint32_t lbo_a = MG * 128, lbo_b = NG * 128, sbo = 128;
+  const uint32_t idesc = instr_desc_tf32(TC_M, NP);  // both operands K-major
+  const uint32_t lbo_a = 16 * 128, lbo_b = (NP / 8) * 128, sbo = 128;
   const int kb = blockIdx.x * ks, ke = min(K, kb + ks);
   uint32_t phase = 0;
   // fp32 round-to-nearest accumulator in smem (row stride NP + 4: conflict-free
@@ -265,71 +272,75 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   int sub0 = kb;
   for (int k0 = kb; k0 < ke; k0 += TC_KC) {
     if (k0 - sub0 >= kSub) sub0 = k0;
-    // lane = K row of the chunk; the warp's MN groups are a quarter of the tile
-    const int kl = lane, k = k0 + kl;
-    const bool kin = k < ke;
-    const int coff = ((kl / 8) * 0 + (kl % 8)) * 4;  // float offset of the K row in a core
-    for (int mg = warp; mg < MG; mg += 4) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kin && mg * 4 < M) v = *reinterpret_cast<const float4*>(A + static_cast<size_t>(k) * M + mg * 4);
+    // A^T chunk: thread t = output row m, 4 K rows per float4 (K-major cores)
+#pragma unroll
+    for (int kc = 0; kc < TC_KC / 4; ++kc) {
+      float w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + kc * 4 + j;
+        w[j] = (t < M && k < ke) ? A[static_cast<size_t>(k) * M + t] : 0.f;
+      }
       float4 h, l;
-      split_tf32(v.x, h.x, l.x);
-      split_tf32(v.y, h.y, l.y);
-      split_tf32(v.z, h.z, l.z);
-      split_tf32(v.w, h.w, l.w);
-      const int off = ((kl / 8) * MG + mg) * 32 + coff;
+      split_tf32(w[0], h.x, l.x);
+      split_tf32(w[1], h.y, l.y);
+      split_tf32(w[2], h.z, l.z);
+      split_tf32(w[3], h.w, l.w);
+      const int off = (kc * 16 + t / 8) * 32 + (t % 8) * 4;
       *reinterpret_cast<float4*>(a_hi + off) = h;
       *reinterpret_cast<float4*>(a_lo + off) = l;
     }
-    for (int ng = warp; ng < NG; ng += 4) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kin) v = *reinterpret_cast<const float4*>(B + static_cast<size_t>(k) * N + ng * 4);
-      float4 h, l;
-      split_tf32(v.x, h.x, l.x);
-      split_tf32(v.y, h.y, l.y);
-      split_tf32(v.z, h.z, l.z);
-      split_tf32(v.w, h.w, l.w);
-      const int off = ((kl / 8) * NG + ng) * 32 + coff;
-      *reinterpret_cast<float4*>(b_hi + off) = h;
-      *reinterpret_cast<float4*>(b_lo + off) = l;
+    // dY chunk: column n of B, 4 K rows per float4 (same layout as the NN kernel)
+    for (int n = t; n < NP; n += TC_THREADS) {
+#pragma unroll
+      for (int kc = 0; kc < TC_KC / 4; ++kc) {
+        float w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + kc * 4 + j;
+          w[j] = (k < ke) ? B[static_cast<size_t>(k) * N + n] : 0.f;
+        }
+        float4 h, l;
+        split_tf32(w[0], h.x, l.x);
+        split_tf32(w[1], h.y, l.y);
+        split_tf32(w[2], h.z, l.z);
+        split_tf32(w[3], h.w, l.w);
+        const int off = (kc * (NP / 8) + n / 8) * 32 + (n % 8) * 4;
+        *reinterpret_cast<float4*>(b_hi + off) = h;
+        *reinterpret_cast<float4*>(b_lo + off) = l;
+      }
     }
-    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (t == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi),
                      bl = smem_u32(b_lo);
 #pragma unroll
       for (int s = 0; s < TC_KC / 8; ++s) {
-        const uint64_t dah = smem_desc(ah + s * lbo_a, lbo_a, sbo), dal = smem_desc(al + s * lbo_a, lbo_a, sbo);
-        const uint64_t dbh = smem_desc(bh + s * lbo_b, lbo_b, sbo), dbl = smem_desc(bl + s * lbo_b, lbo_b, sbo);
+        const uint32_t da = s * 2 * lbo_a, db = s * 2 * lbo_b;
+        const uint64_t dah = smem_desc(ah + da, lbo_a, sbo), dal = smem_desc(al + da, lbo_a, sbo);
+        const uint64_t dbh = smem_desc(bh + db, lbo_b, sbo), dbl = smem_desc(bl + db, lbo_b, sbo);
         mma_tf32(tmem, dah, dbh, idesc, (k0 > sub0 || s > 0) ? 1u : 0u);
         mma_tf32(tmem, dah, dbl, idesc, 1u);
         mma_tf32(tmem, dal, dbh, idesc, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&mbar)));
+          smem_u32(&mbar)) : "memory");
     }
     mbar_wait(smem_u32(&mbar), phase);
     phase ^= 1;
     const int nk = k0 + TC_KC;
     if (nk >= ke || nk - sub0 >= kSub) {  // drain this sub-slice: TMEM -> smem (RN adds)
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int c = 0; c < NP; c += 16) {
         uint32_t r[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-              "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
-              "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(tmem + lane_base + c));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        tmem_ld16(tmem + lane_base + c, r);
         float* a = acc_s + t * AS + c;
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] += __uint_as_float(r[j]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();  // TMEM reads complete before the next sub-slice's MMAs
     }
   }
@@ -342,7 +353,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         *reinterpret_cast<float4*>(dst + c + j) = *reinterpret_cast<const float4*>(acc_s + t * AS + c + j);
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
