@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--cta-threshold", type=int, default=0)
     ap.add_argument("--no-layer", action="store_true",
                     help="skip the layer-level (projection + pipeline) measurement")
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the forward fusion-strategy ablation (smmf/pmf/unfused/baseline)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args()
@@ -400,6 +402,40 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush):
             "projection_fwd_ms": seg(0), "pipeline_ms": seg(1), "weight_grad_ms": seg(2),
             "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; X^T*dY deterministic split-K)",
             "x_width": F}
+
+
+def strategy_ablation(dg, spec, Q, K, V, O, stats, stream, flush, steps=5):
+    """Forward time per fusion strategy (the paper's ablation, DF-GNN §5):
+    SMMF (this design's default), PMF, unfused and the feature-parallel
+    baseline, each on the same inputs with L2 flushed before every launch
+    group; CUDA events on the launching stream."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    out = {}
+    for strat in ("smmf", "pmf", "unfused", "baseline"):
+        try:
+            ws = fused.strategy_workspace(dg, spec, strat, dtype=V.dtype, device=V.device)
+            for _ in range(2):
+                fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream,
+                                   strategy=strat, workspace=ws)
+            ms = []
+            for _ in range(steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream,
+                                   strategy=strat, workspace=ws)
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+            out[strat] = round(statistics.mean(ms), 4)
+            del ws
+        except Exception as ex:  # reported, never silently replaced
+            out[strat] = f"failed: {ex}"
+    torch.cuda.synchronize()
+    return out
 
 
 def run_ours(args, rank, world):
@@ -581,6 +617,9 @@ def run_ours(args, rank, world):
     layer_out = None
     if not sharded and not args.no_layer:
         layer_out = layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush)
+    ablation = None
+    if not sharded and not args.no_ablation:
+        ablation = strategy_ablation(dg, spec, Q, K, V, O, stats, stream, flush)
 
     # ---- roofline of the dominant kernel
     means = {"fwd": statistics.mean(k_fwd), "bwd_rows": statistics.mean(k_ra),
@@ -638,6 +677,7 @@ def run_ours(args, rank, world):
             "e2e": {"value": e2e_val, "unit": "GEdges/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "layer": layer_out,
+            "fwd_strategy_ms": ablation,
             "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
         }

@@ -54,6 +54,12 @@ extern "C" {
 #define GF_DOT 0 /* SddmmVariant::Dot (GT, AGNN) */
 #define GF_ADD 1 /* SddmmVariant::Add (GAT) */
 
+/* Fusion strategies (reference Strategy enum, schedule.hpp:12-18). */
+#define GF_STRAT_SMMF 0     /* 1 launch, fused, nothing E x H in HBM (default)      */
+#define GF_STRAT_PMF 1      /* edge-parallel SDDMM -> S[E x H]; fused softmax+SpMM  */
+#define GF_STRAT_UNFUSED 2  /* SDDMM -> S; softmax -> P[E x H]; SpMM: 3 launches    */
+#define GF_STRAT_BASELINE 3 /* feature-parallel fused kernel, rows in id order      */
+
 typedef struct gf_graph_s* gf_graph_t;
 
 /* Attention operator descriptor: SddmmKind (dense.hpp:48-62) + head shape. */
@@ -138,6 +144,19 @@ int gf_graph_get_schedule(gf_graph_t g, int32_t* row_order, int32_t* col_order);
  * ForwardContext::P). */
 int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                 const void* V, void* O, void* stats, void* P, void* stream);
+
+/* ---- forward under an explicit fusion strategy (run_smmf / run_pmf /
+ * run_unfused / run_feature_parallel_baseline, engine.hpp:292-329) ----
+ * Same outputs as gf_attn_fwd (O, the softmax records, P when non-NULL) for
+ * every strategy; they differ in launch structure and HBM traffic only.
+ * PMF and unfused need E*H (unfused without P: 2*E*H) elements of scratch:
+ * gf_attn_fwd_workspace reports the bytes; workspace == NULL makes the call
+ * allocate (stream-ordered) and free it itself. */
+int gf_attn_fwd_workspace(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy,
+                          int32_t have_p, size_t* bytes);
+int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy, const void* Q,
+                         const void* K, const void* V, void* O, void* stats, void* P,
+                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
  * Pass A over CSR rows (dK or der, and delta into stats), pass B over CSC

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("GF_CUDA_LIB") or os.path.join(_HERE, "libgraphfuse_cu
 GF_OK = 0
 GF_F32, GF_F64 = 0, 1
 GF_DOT, GF_ADD = 0, 1
+GF_STRAT = {"smmf": 0, "pmf": 1, "unfused": 2, "baseline": 3}
 
 _vp = C.c_void_p
 
@@ -56,6 +57,10 @@ SIGNATURES = {
     "gf_graph_get_info": (C.c_int, [_vp, C.POINTER(GraphInfo)]),
     "gf_graph_get_schedule": (C.c_int, [_vp, _vp, _vp]),
     "gf_attn_fwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gf_attn_fwd_workspace": (C.c_int, [_vp, C.POINTER(AttnDesc), C.c_int32, C.c_int32,
+                                        C.POINTER(C.c_size_t)]),
+    "gf_attn_fwd_strategy": (C.c_int, [_vp, C.POINTER(AttnDesc), C.c_int32, _vp, _vp, _vp, _vp,
+                                       _vp, _vp, _vp, C.c_size_t, _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp]),
     "gf_attn_bwd_rows": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,

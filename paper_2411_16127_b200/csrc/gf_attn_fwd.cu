@@ -37,7 +37,10 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
   m = mn;
 }
 
-template <typename T, int CB, int LPE, int CPL, int VAR>
+// MODE 0: SMMF (scores computed here); 1: PMF's fused softmax + SpMM over the
+// scores an edge-parallel SDDMM wrote to a.ES; 2: the unfused SpMM (a.ES holds
+// normalised probabilities: O = sum p V, no softmax, no records).
+template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
@@ -62,11 +65,15 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
   const T* __restrict__ Vb = a.V + off;
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
+  const T* __restrict__ Sb = a.ES + h;        // MODE 1/2: ES[e * H + h]
 
   // Destination-side operands stay in registers for the whole row.
   T kv[NE];
   T erv = T(0), rk = T(1);
-  if constexpr (VAR == GF_DOT) {
+  if constexpr (MODE == 2) {
+    // probabilities given: no destination-side score operands
+  } else if constexpr (VAR == GF_DOT) {
+    if (MODE == 0 || a.l2) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       ld_own<T, CB>(a.K + static_cast<size_t>(v) * a.F + off + k * CW,
@@ -76,6 +83,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
       for (int i = 0; i < NE; ++i) s += kv[i] * kv[i];
       rk = inv_norm(head_sum(s, a.LPH));
+    }
     }
   } else {
     erv = __ldg(a.K + static_cast<size_t>(v) * a.H + h);
@@ -103,7 +111,9 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
           ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
-        if constexpr (VAR == GF_DOT) {
+        if constexpr (MODE != 0) {
+          s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(base + j) * a.H) : T(0);
+        } else if constexpr (VAR == GF_DOT) {
 #pragma unroll
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
@@ -111,10 +121,20 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
           s[t] = ld_node(Qb + uu * qs);
         }
       }
+      if constexpr (MODE == 2) {
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+#pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
+        }
+        continue;
+      }
       T smax = ninf<T>();
 #pragma unroll
       for (int t = 0; t < U; ++t) {
-        if constexpr (VAR == GF_DOT) {
+        if constexpr (MODE == 1) {
+          // score read from ES
+        } else if constexpr (VAR == GF_DOT) {
           T d = T(0), qq = T(0);
 #pragma unroll
           for (int i = 0; i < NE; ++i) {
@@ -158,7 +178,12 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
     for (int i = 0; i < NE; ++i) acc2[i] = __shfl_xor_sync(kFull, acc[i], o);
     const T m2 = __shfl_xor_sync(kFull, m, o);
     const T l2 = __shfl_xor_sync(kFull, l, o);
-    merge_state<T, NE>(m, l, acc, m2, l2, acc2);
+    if constexpr (MODE == 2) {
+#pragma unroll
+      for (int i = 0; i < NE; ++i) acc[i] += acc2[i];
+    } else {
+      merge_state<T, NE>(m, l, acc, m2, l2, acc2);
+    }
   }
 
   if (cta) {
@@ -184,13 +209,18 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
         T acc2[NE];
 #pragma unroll
         for (int i = 0; i < NE; ++i) acc2[i] = d[2 + i];
-        merge_state<T, NE>(m, l, acc, d[0], d[1], acc2);
+        if constexpr (MODE == 2) {
+#pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] += acc2[i];
+        } else {
+          merge_state<T, NE>(m, l, acc, d[0], d[1], acc2);
+        }
       }
     }
   }
 
   if (sub == 0) {
-    const T r = l == T(0) ? T(0) : T(1) / l;
+    const T r = MODE == 2 ? T(1) : (l == T(0) ? T(0) : T(1) / l);
     T o[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) o[i] = acc[i] * r;
@@ -198,7 +228,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       st_chunk<T, CB>(orow + k * CW, *reinterpret_cast<T(*)[CW]>(o + k * CW));
-    if (c % a.LPH == 0) {
+    if (MODE != 2 && c % a.LPH == 0) {
       T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + h);
       rec[0] = l == T(0) ? ninf<T>() : m;
       rec[1] = l == T(0) ? T(0) : lg2(l);
@@ -211,7 +241,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 // Any (H <= 32, D): warp per row, two passes (max, then exp/sum/aggregate),
 // per-head scalars owned by lane h, feature accumulators in shared memory.
 // Used for shapes whose head does not tile into 16-byte chunks (e.g. D = 5).
-template <typename T, int VAR>
+template <typename T, int VAR, int MODE = 0>
 __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -232,17 +262,25 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   T erh, rkh;
   generic_row_setup<T, VAR>(a, v, lane, VAR == GF_DOT ? kvs : nullptr, erh, rkh);
   T m = ninf<T>(), l = T(0);
-  for (int i = eb; i < ee; ++i) {
-    const int u = __ldg(a.idx + i);
-    if (lane < a.H) {
-      const T s = generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh);
-      m = (m < s || i == eb) ? s : m;  // left-to-right max from the first edge
+  if (MODE != 2) {
+    for (int i = eb; i < ee; ++i) {
+      if (lane < a.H) {
+        const T s = MODE == 1 ? ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane)
+                              : generic_score<T, VAR>(a, __ldg(a.idx + i), v, lane, kvs, erh, rkh);
+        m = (m < s || i == eb) ? s : m;  // left-to-right max from the first edge
+      }
     }
   }
   for (int i = eb; i < ee; ++i) {
     const int u = __ldg(a.idx + i);
     if (lane < a.H) {
-      const T p = expd(generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh) - m);
+      T p;
+      if constexpr (MODE == 2)
+        p = ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane);
+      else if constexpr (MODE == 1)
+        p = expd(ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane) - m);
+      else
+        p = expd(generic_score<T, VAR>(a, u, v, lane, kvs, erh, rkh) - m);
       l += p;
       ph[lane] = p;
     }
@@ -251,7 +289,9 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
       acc[f] += ph[f / a.D] * __ldg(a.V + static_cast<size_t>(u) * a.F + f);
     __syncwarp();
   }
-  if (lane < a.H) {
+  if (MODE == 2) {
+    if (lane < a.H) lh[lane] = T(1);
+  } else if (lane < a.H) {
     lh[lane] = l;
     T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + lane);
     rec[0] = l == T(0) ? ninf<T>() : m;
@@ -261,7 +301,8 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   __syncwarp();
   for (int f = lane; f < a.F; f += 32) {
     const T lv = lh[f / a.D];
-    a.O[static_cast<size_t>(v) * a.F + f] = lv == T(0) ? T(0) : acc[f] / lv;
+    a.O[static_cast<size_t>(v) * a.F + f] =
+        MODE == 2 ? acc[f] : (lv == T(0) ? T(0) : acc[f] / lv);
   }
 }
 
@@ -284,8 +325,14 @@ __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __re
 }
 
 template <typename T, int CB, int LPE, int CPL>
-int launch_fast_fwd(const FwdArgs<T>& a, int variant, int blocks, cudaStream_t s) {
-  if (variant == GF_DOT)
+int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cudaStream_t s) {
+  if (mode == 2)  // probabilities given: the score variant is irrelevant
+    fwd_fast<T, CB, LPE, CPL, GF_ADD, 2><<<blocks, 256, 0, s>>>(a);
+  else if (mode == 1 && variant == GF_DOT)
+    fwd_fast<T, CB, LPE, CPL, GF_DOT, 1><<<blocks, 256, 0, s>>>(a);
+  else if (mode == 1)
+    fwd_fast<T, CB, LPE, CPL, GF_ADD, 1><<<blocks, 256, 0, s>>>(a);
+  else if (variant == GF_DOT)
     fwd_fast<T, CB, LPE, CPL, GF_DOT><<<blocks, 256, 0, s>>>(a);
   else
     fwd_fast<T, CB, LPE, CPL, GF_ADD><<<blocks, 256, 0, s>>>(a);
@@ -320,6 +367,24 @@ static bool aligned(const void* p, int b) { return (reinterpret_cast<uintptr_t>(
 
 template <typename T>
 int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_t s) {
+  return launch_fwd_mode<T>(g, a0, variant, 0, s);
+}
+
+template <typename T, int VAR, int MODE>
+int launch_generic(const FwdArgs<T>& a, size_t smem, cudaStream_t s) {
+  if (smem > 48 * 1024)
+    GF_CHECK_CUDA(cudaFuncSetAttribute(fwd_generic<T, VAR, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+  const int blocks = (a.n + kGenericWarps - 1) / kGenericWarps;
+  fwd_generic<T, VAR, MODE><<<blocks, 32 * kGenericWarps, smem, s>>>(a);
+  GF_CHECK_LAUNCH("fwd_generic");
+  return GF_OK;
+}
+
+template <typename T>
+int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mode,
+                    cudaStream_t s) {
   if (g.n == 0) return GF_OK;
   FwdArgs<T> a = a0;
   if (a.n == 0) return GF_OK;  // every row skipped (row-sharded graph)
@@ -327,31 +392,31 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_
   const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
   const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
                   aligned(a.stats, 32) &&
-                  (variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
+                  (mode == 2 || variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
   if (al) {
     a.LPH = fs.lph;
     const int warp_rows = a.n - a.n_cta;
     const int blocks = a.n_cta + (warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;
     switch (key) {
-      case 32011: return launch_fast_fwd<T, 32, 1, 1>(a, variant, blocks, s);
-      case 32021: return launch_fast_fwd<T, 32, 2, 1>(a, variant, blocks, s);
-      case 32041: return launch_fast_fwd<T, 32, 4, 1>(a, variant, blocks, s);
-      case 32081: return launch_fast_fwd<T, 32, 8, 1>(a, variant, blocks, s);
-      case 32161: return launch_fast_fwd<T, 32, 16, 1>(a, variant, blocks, s);
-      case 32321: return launch_fast_fwd<T, 32, 32, 1>(a, variant, blocks, s);
-      case 32012: return launch_fast_fwd<T, 32, 1, 2>(a, variant, blocks, s);
-      case 32022: return launch_fast_fwd<T, 32, 2, 2>(a, variant, blocks, s);
-      case 32042: return launch_fast_fwd<T, 32, 4, 2>(a, variant, blocks, s);
-      case 32082: return launch_fast_fwd<T, 32, 8, 2>(a, variant, blocks, s);
-      case 32162: return launch_fast_fwd<T, 32, 16, 2>(a, variant, blocks, s);
-      case 32322: return launch_fast_fwd<T, 32, 32, 2>(a, variant, blocks, s);
-      case 16011: return launch_fast_fwd<T, 16, 1, 1>(a, variant, blocks, s);
-      case 16021: return launch_fast_fwd<T, 16, 2, 1>(a, variant, blocks, s);
-      case 16041: return launch_fast_fwd<T, 16, 4, 1>(a, variant, blocks, s);
-      case 16081: return launch_fast_fwd<T, 16, 8, 1>(a, variant, blocks, s);
-      case 16161: return launch_fast_fwd<T, 16, 16, 1>(a, variant, blocks, s);
-      case 16321: return launch_fast_fwd<T, 16, 32, 1>(a, variant, blocks, s);
+      case 32011: return launch_fast_fwd<T, 32, 1, 1>(a, variant, mode, blocks, s);
+      case 32021: return launch_fast_fwd<T, 32, 2, 1>(a, variant, mode, blocks, s);
+      case 32041: return launch_fast_fwd<T, 32, 4, 1>(a, variant, mode, blocks, s);
+      case 32081: return launch_fast_fwd<T, 32, 8, 1>(a, variant, mode, blocks, s);
+      case 32161: return launch_fast_fwd<T, 32, 16, 1>(a, variant, mode, blocks, s);
+      case 32321: return launch_fast_fwd<T, 32, 32, 1>(a, variant, mode, blocks, s);
+      case 32012: return launch_fast_fwd<T, 32, 1, 2>(a, variant, mode, blocks, s);
+      case 32022: return launch_fast_fwd<T, 32, 2, 2>(a, variant, mode, blocks, s);
+      case 32042: return launch_fast_fwd<T, 32, 4, 2>(a, variant, mode, blocks, s);
+      case 32082: return launch_fast_fwd<T, 32, 8, 2>(a, variant, mode, blocks, s);
+      case 32162: return launch_fast_fwd<T, 32, 16, 2>(a, variant, mode, blocks, s);
+      case 32322: return launch_fast_fwd<T, 32, 32, 2>(a, variant, mode, blocks, s);
+      case 16011: return launch_fast_fwd<T, 16, 1, 1>(a, variant, mode, blocks, s);
+      case 16021: return launch_fast_fwd<T, 16, 2, 1>(a, variant, mode, blocks, s);
+      case 16041: return launch_fast_fwd<T, 16, 4, 1>(a, variant, mode, blocks, s);
+      case 16081: return launch_fast_fwd<T, 16, 8, 1>(a, variant, mode, blocks, s);
+      case 16161: return launch_fast_fwd<T, 16, 16, 1>(a, variant, mode, blocks, s);
+      case 16321: return launch_fast_fwd<T, 16, 32, 1>(a, variant, mode, blocks, s);
       default: break;
     }
   }
@@ -364,22 +429,12 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a0, int variant, cudaStream_
     set_error("gf_attn_fwd: feature width too large for the generic path");
     return GF_ERR_UNSUPPORTED;
   }
-  const int blocks = (a.n + kGenericWarps - 1) / kGenericWarps;
-  if (variant == GF_DOT) {
-    if (smem > 48 * 1024)
-      GF_CHECK_CUDA(cudaFuncSetAttribute(fwd_generic<T, GF_DOT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    fwd_generic<T, GF_DOT><<<blocks, 32 * kGenericWarps, smem, s>>>(a);
-  } else {
-    if (smem > 48 * 1024)
-      GF_CHECK_CUDA(cudaFuncSetAttribute(fwd_generic<T, GF_ADD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    fwd_generic<T, GF_ADD><<<blocks, 32 * kGenericWarps, smem, s>>>(a);
-  }
-  GF_CHECK_LAUNCH("fwd_generic");
-  return GF_OK;
+  if (mode == 2) return launch_generic<T, GF_ADD, 2>(a, smem, s);
+  if (mode == 1)
+    return variant == GF_DOT ? launch_generic<T, GF_DOT, 1>(a, smem, s)
+                             : launch_generic<T, GF_ADD, 1>(a, smem, s);
+  return variant == GF_DOT ? launch_generic<T, GF_DOT, 0>(a, smem, s)
+                           : launch_generic<T, GF_ADD, 0>(a, smem, s);
 }
 
 template <typename T>
@@ -400,6 +455,9 @@ int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T*
 }
 
 template int launch_fwd<float>(const DevGraph&, const FwdArgs<float>&, int, cudaStream_t);
+template int launch_fwd_mode<float>(const DevGraph&, const FwdArgs<float>&, int, int, cudaStream_t);
+template int launch_fwd_mode<double>(const DevGraph&, const FwdArgs<double>&, int, int,
+                                     cudaStream_t);
 template int launch_fwd<double>(const DevGraph&, const FwdArgs<double>&, int, cudaStream_t);
 template int launch_materialize_p<float>(const DevGraph&, const FwdArgs<float>&, int, float*,
                                          cudaStream_t);

@@ -152,6 +152,58 @@ extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q
                                : fwd_impl<double>(g, *desc, Q, K, V, O, stats, P, s);
 }
 
+extern "C" int gf_attn_fwd_workspace(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy,
+                                     int32_t have_p, size_t* bytes) {
+  if (int rc = check_desc(desc, "gf_attn_fwd_workspace")) return rc;
+  if (bad_graph(g, "gf_attn_fwd_workspace")) return GF_ERR_INVALID;
+  if (!bytes || strategy < GF_STRAT_SMMF || strategy > GF_STRAT_BASELINE) {
+    gfb::set_error("gf_attn_fwd_workspace: invalid arguments");
+    return GF_ERR_INVALID;
+  }
+  *bytes = gfb::strategy_workspace_bytes(*g, desc->heads, desc->dtype == GF_F32 ? 4 : 8, strategy,
+                                         have_p != 0);
+  return GF_OK;
+}
+
+extern "C" int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy,
+                                    const void* Q, const void* K, const void* V, void* O,
+                                    void* stats, void* P, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  if (int rc = check_desc(desc, "gf_attn_fwd_strategy")) return rc;
+  if (bad_graph(g, "gf_attn_fwd_strategy")) return GF_ERR_INVALID;
+  if (strategy < GF_STRAT_SMMF || strategy > GF_STRAT_BASELINE) {
+    gfb::set_error("gf_attn_fwd_strategy: unknown strategy");
+    return GF_ERR_INVALID;
+  }
+  if (g->n > 0 && (!Q || !K || !V || !O || !stats)) {
+    gfb::set_error("gf_attn_fwd_strategy: null operand");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  const int elem = desc->dtype == GF_F32 ? 4 : 8;
+  const size_t need = gfb::strategy_workspace_bytes(*g, desc->heads, elem, strategy, P != nullptr);
+  void* ws = workspace;
+  bool own = false;
+  if (need > 0 && !ws) {
+    GF_CHECK_CUDA(cudaMallocAsync(&ws, need, s));
+    own = true;
+  } else if (need > workspace_bytes) {
+    gfb::set_error("gf_attn_fwd_strategy: workspace too small (see gf_attn_fwd_workspace)");
+    return GF_ERR_INVALID;
+  }
+  int rc;
+  if (desc->dtype == GF_F32)
+    rc = gfb::launch_fwd_strategy<float>(*g, fwd_args<float>(*g, *desc, Q, K, V, O, stats),
+                                         desc->variant, strategy, static_cast<float*>(P),
+                                         static_cast<float*>(ws), s);
+  else
+    rc = gfb::launch_fwd_strategy<double>(*g, fwd_args<double>(*g, *desc, Q, K, V, O, stats),
+                                          desc->variant, strategy, static_cast<double*>(P),
+                                          static_cast<double*>(ws), s);
+  if (own) cudaFreeAsync(ws, s);
+  return rc;
+}
+
 extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                            const void* V, const void* O, void* stats, const void* dO, void* dQ,
                            void* dK, void* dV, void* stream) {

@@ -51,6 +51,18 @@ __device__ __forceinline__ int ld_idx(const int32_t* __restrict__ p) {
 #endif
 }
 
+/// Streamed edge value (E x H score / probability buffers of the
+/// non-fused strategies; read once per pass).
+template <typename T>
+__device__ __forceinline__ T ld_edge(const T* __restrict__ p) {
+  T v;
+  if constexpr (sizeof(T) == 4)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_stream()));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_stream()));
+  return v;
+}
+
 /// Gathered scalar of a node table (el[src], ...).
 template <typename T>
 __device__ __forceinline__ T ld_node(const T* __restrict__ p) {

@@ -122,6 +122,7 @@ void free_graph(DevGraph* g) {
   cudaFree(g->csc_row);
   cudaFree(g->row_order);
   cudaFree(g->col_order);
+  cudaFree(g->coo_dst);
   delete g;
 }
 

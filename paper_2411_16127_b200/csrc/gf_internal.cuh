@@ -50,6 +50,8 @@ struct DevGraph {
   int32_t n_cta_cols = 0, n_empty_cols = 0;
   int64_t max_in = 0, max_out = 0;
   int device = 0;
+  int32_t* coo_dst = nullptr;  // CSR-order destination per edge (built on first use by
+                               // the edge-parallel strategies; graph-owned)
   int32_t e_csc = 0;        // CSC edge count (== e unless row-sharded)
   bool skip_empty = false;  // do not visit rows / columns without edges
   /// Rows (resp. columns) a pass visits: the empty ones trail the order.
@@ -108,6 +110,7 @@ struct FwdArgs {
   const T* V;
   T* O;
   T* stats;  // N x H x 4 records (gf_device.cuh Rec)
+  const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
 };
 
 template <typename T>
@@ -136,6 +139,17 @@ int launch_fwd(const DevGraph& g, const FwdArgs<T>& a, int variant, cudaStream_t
 template <typename T>
 int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T* P,
                          cudaStream_t s);
+// Forward kernel modes: 0 = SMMF (compute scores), 1 = scores read from ES
+// (PMF's fused softmax + SpMM), 2 = probabilities read from ES (unfused SpMM:
+// no softmax, O = sum p V, no records).
+template <typename T>
+int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a, int variant, int mode, cudaStream_t s);
+// Fusion strategies (gf_attn_strategies.cu).  ws: E*H (PMF) or 2*E*H
+// (unfused without caller P) elements of scratch.
+size_t strategy_workspace_bytes(const DevGraph& g, int heads, int elem, int strategy, bool have_p);
+template <typename T>
+int launch_fwd_strategy(DevGraph& g, const FwdArgs<T>& a, int variant, int strategy, T* P, T* ws,
+                        cudaStream_t s);
 // passes: bit 0 = pass A (CSR rows), bit 1 = pass B (CSC columns).
 template <typename T>
 int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStream_t s);

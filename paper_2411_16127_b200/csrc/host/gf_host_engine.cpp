@@ -122,11 +122,21 @@ void validate_inputs(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<
     throw KernelError("engine: el/er must have N rows");
 }
 
-/// Device forward: returns O and lse (and P when want_p).
+int strategy_code(Strategy s) {
+  switch (s) {
+    case Strategy::Pmf: return GF_STRAT_PMF;
+    case Strategy::Unfused: return GF_STRAT_UNFUSED;
+    case Strategy::FeatureParallelBaseline: return GF_STRAT_BASELINE;
+    default: return GF_STRAT_SMMF;
+  }
+}
+
+/// Device forward under `mode`'s kernels: returns O and lse (and P when want_p).
 template <typename T>
 void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>& Q,
                     const DenseMatrix<T>& K, const DenseMatrix<T>& V, const SddmmKind& kind,
-                    std::vector<T>& O, std::vector<T>& lse, std::vector<T>* P) {
+                    std::vector<T>& O, std::vector<T>& lse, std::vector<T>* P,
+                    Strategy mode = Strategy::Smmf) {
   gf_graph_t dg = device_graph(g, plan);
   const std::int64_t d = V.cols;
   const gf_attn_desc desc = make_desc<T>(kind, d);
@@ -135,7 +145,8 @@ void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>
   lse.assign(static_cast<size_t>(4 * g.num_nodes), T(0));  // softmax records (4 per row)
   DevBuf dO(sizeof(T) * O.size()), dl(sizeof(T) * lse.size());
   DevBuf dp(P ? sizeof(T) * static_cast<size_t>(g.num_edges) : 0);
-  GFH_CALL(gf_attn_fwd(dg, &desc, dq.p, dk.p, dv.p, dO.p, dl.p, P ? dp.p : nullptr, nullptr));
+  GFH_CALL(gf_attn_fwd_strategy(dg, &desc, strategy_code(mode), dq.p, dk.p, dv.p, dO.p, dl.p,
+                                P ? dp.p : nullptr, nullptr, 0, nullptr));
   GFH_CALL(gf_stream_sync(nullptr));
   dO.to(O);
   dl.to(lse);
@@ -160,7 +171,7 @@ ForwardResult<T> run_mode(const Graph& g, const DenseMatrix<T>& Q, const DenseMa
   res.ctx.V = V;
   res.ctx.kind = kind;
   res.ctx.plan = plan.with_strategy(mode);
-  device_forward(g, plan, Q, K, V, kind, res.ctx.O, res.ctx.lse, &res.ctx.P.values);
+  device_forward(g, plan, Q, K, V, kind, res.ctx.O, res.ctx.lse, &res.ctx.P.values, mode);
   res.O = DenseMatrix<T>(g.num_nodes, d);
   res.O.data = res.ctx.O;
   res.counters = model_counters<T>(g, kind, plan, d, mode);

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._capi import AttnDesc, GraphInfo, check, lib
+from ._capi import GF_STRAT, AttnDesc, GraphInfo, check, lib
 
 DTYPES = {torch.float32: _capi.GF_F32, torch.float64: _capi.GF_F64}
 
@@ -136,10 +136,13 @@ def from_coo_device(n: int, src: torch.Tensor, dst: torch.Tensor, stream=None):
 
 
 def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, stats=None,
-                 stream=None):
-    """One fused launch; returns (O, stats) or (O, stats, P).
+                 stream=None, strategy="smmf", workspace=None):
+    """Forward; returns (O, stats) or (O, stats, P).
 
-    stats is N x H x 4 softmax records {m, log2 l, aux, delta} (gf_cuda.h)."""
+    strategy "smmf" (default) is the one fused launch; "pmf", "unfused" and
+    "baseline" run the reference Strategy's launch structure (gf_cuda.h
+    GF_STRAT_*).  stats is N x H x 4 softmax records {m, log2 l, aux, delta}
+    (gf_cuda.h).  workspace: optional preallocated scratch (strategy_workspace)."""
     n = g.n
     dt = V.dtype
     if O is None:
@@ -148,9 +151,24 @@ def attn_forward(g: DeviceGraph, spec: AttnSpec, Q, K, V, want_p=False, O=None, 
         stats = torch.empty(n, spec.heads, 4, dtype=dt, device=V.device)
     P = torch.empty(max(g.e, 1), spec.heads, dtype=dt, device=V.device) if want_p else None
     d = spec.desc(dt)
-    check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats), _p(P),
-                            _stream(stream)), "gf_attn_fwd")
+    if strategy == "smmf" and workspace is None:
+        check(lib().gf_attn_fwd(g.handle, C.byref(d), _p(Q), _p(K), _p(V), _p(O), _p(stats),
+                                _p(P), _stream(stream)), "gf_attn_fwd")
+    else:
+        ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        check(lib().gf_attn_fwd_strategy(g.handle, C.byref(d), GF_STRAT[strategy], _p(Q), _p(K),
+                                         _p(V), _p(O), _p(stats), _p(P), _p(workspace), ws_bytes,
+                                         _stream(stream)), "gf_attn_fwd_strategy")
     return (O, stats, P[: g.e]) if want_p else (O, stats)
+
+
+def strategy_workspace(g: DeviceGraph, spec: AttnSpec, strategy: str, dtype=torch.float32,
+                       device="cuda", want_p=False):
+    """Scratch buffer for attn_forward(strategy=...) (None when none is needed)."""
+    n = C.c_size_t()
+    check(lib().gf_attn_fwd_workspace(g.handle, C.byref(spec.desc(dtype)), GF_STRAT[strategy],
+                                      int(want_p), C.byref(n)), "gf_attn_fwd_workspace")
+    return torch.empty(n.value, dtype=torch.uint8, device=device) if n.value else None
 
 
 def lse_of(stats):

@@ -62,7 +62,7 @@ def make_inputs(g, variant, H, D, dtype, seed):
     return Q, K, V, dO
 
 
-def run_device(g, spec, Q, K, V, dO, cta_threshold=0, want_p=False):
+def run_device(g, spec, Q, K, V, dO, cta_threshold=0, want_p=False, strategy="smmf"):
     import torch
 
     from paper_2411_16127_b200 import fused
@@ -71,7 +71,7 @@ def run_device(g, spec, Q, K, V, dO, cta_threshold=0, want_p=False):
                                          cta_threshold=cta_threshold)
     dev = torch.device("cuda:0")
     t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (Q, K, V, dO)]
-    out = fused.attn_forward(dg, spec, t[0], t[1], t[2], want_p=want_p)
+    out = fused.attn_forward(dg, spec, t[0], t[1], t[2], want_p=want_p, strategy=strategy)
     O, stats = out[0], out[1]
     dQ, dK, dV = fused.attn_backward(dg, spec, t[0], t[1], t[2], O, stats, t[3])
     torch.cuda.synchronize()
@@ -82,13 +82,15 @@ def run_device(g, spec, Q, K, V, dO, cta_threshold=0, want_p=False):
     return res
 
 
-def check_against_oracle(g, variant, l2, H, D, dtype, seed=1, cta_threshold=0, scale=None):
+def check_against_oracle(g, variant, l2, H, D, dtype, seed=1, cta_threshold=0, scale=None,
+                         strategy="smmf"):
     from paper_2411_16127_b200.fused import AttnSpec
 
     scale = (1.0 / np.sqrt(D)) if scale is None else scale
     spec = AttnSpec(variant=variant, heads=H, head_dim=D, scale=scale, slope=0.2, l2=l2)
     Q, K, V, dO = make_inputs(g, variant, H, D, dtype, seed)
-    got = run_device(g, spec, Q, K, V, dO, cta_threshold=cta_threshold, want_p=True)
+    got = run_device(g, spec, Q, K, V, dO, cta_threshold=cta_threshold, want_p=True,
+                     strategy=strategy)
     O, P, lse = oracle.forward(g, Q, K, V, H, D, variant, l2, scale, 0.2, want_p=True,
                                want_lse=True)
     dQ, dK, dV = oracle.backward(g, Q, K, V, dO, H, D, variant, l2, scale, 0.2)
@@ -99,7 +101,7 @@ def check_against_oracle(g, variant, l2, H, D, dtype, seed=1, cta_threshold=0, s
     errs["lse"] = rel_err(got["lse"][finite], lse[finite])
     assert np.all(np.isneginf(got["lse"][~finite])), "empty rows must carry lse = -inf"
     bad = {k: v for k, v in errs.items() if not v <= tol}
-    assert not bad, f"{variant} l2={l2} H={H} D={D} {dtype.__name__}: {errs}"
+    assert not bad, f"{strategy} {variant} l2={l2} H={H} D={D} {dtype.__name__}: {errs}"
     return errs
 
 
@@ -138,6 +140,28 @@ def test_super_rows_edge_split(cuda, cfg, thr):
     variant, l2, H, D, dt = cfg
     for name in ("hub", "powerlaw"):
         check_against_oracle(make_graph(name), variant, l2, H, D, dt, cta_threshold=thr)
+
+
+@pytest.mark.parametrize("strategy", ["pmf", "unfused", "baseline"])
+@pytest.mark.parametrize("cfg", CONFIGS, ids=lambda c: f"{c[0]}{'-l2' if c[1] else ''}-{c[2]}x{c[3]}-{c[4].__name__}")
+def test_strategy_parity(cuda, cfg, strategy):
+    """The non-default Strategy kernels (PMF: edge-parallel SDDMM + fused
+    softmax/SpMM; unfused: SDDMM -> softmax -> SpMM; feature-parallel
+    baseline) match the oracle like SMMF, including hub and empty rows, and
+    their softmax records drive the same recompute backward."""
+    variant, l2, H, D, dt = cfg
+    if strategy == "baseline" and H * D > 256:
+        from paper_2411_16127_b200 import fused
+        from paper_2411_16127_b200._capi import GFError
+
+        g = make_graph("random")
+        spec = fused.AttnSpec(variant=variant, heads=H, head_dim=D, scale=1.0, slope=0.2, l2=l2)
+        with pytest.raises(GFError, match="H\\*D <= 256"):
+            run_device(g, spec, *make_inputs(g, variant, H, D, dt, 1), strategy=strategy)
+        return
+    for name in ("random", "sparse_empty", "hub"):
+        check_against_oracle(make_graph(name), variant, l2, H, D, dt, strategy=strategy,
+                             cta_threshold=16 if name == "hub" else 0)
 
 
 def test_reference_direct(cuda):
