@@ -158,6 +158,14 @@ int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strateg
                          const void* K, const void* V, void* O, void* stats, void* P,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* Device time of the strategy's forward on resident inputs: one warm-up call,
+ * then `reps` calls bracketed by CUDA events on `stream`; *ms_out = mean ms
+ * per forward.  Synchronises `stream`.  (The bench harness, run_benchmark,
+ * reports this measured GPU time next to the reference's modelled counters.) */
+int gf_time_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy, const void* Q,
+                         const void* K, const void* V, void* O, void* stats, int32_t reps,
+                         float* ms_out, void* stream);
+
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
  * Pass A over CSR rows (dK or der, and delta into stats), pass B over CSC
  * columns (dQ or del, dV).  Attention is recomputed from the stats records;

@@ -23,7 +23,12 @@ INC = os.path.join(ROOT, "include")
 OBJ = os.path.join(ROOT, "build", "obj")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CXX = os.environ.get("CXX", "g++")
+# The host libraries must share the process's libstdc++ (torch loads the
+# system libstdc++.so): a toolchain that links libstdc++ statically (this
+# image's CXX wrapper does) would export a second copy of the locale/iostream
+# internals and crash std::ostream use once torch is imported.  Prefer the
+# system g++; GF_CXX overrides.
+CXX = os.environ.get("GF_CXX") or ("/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", f"-I{INC}", f"-I{CSRC}"]

@@ -61,6 +61,8 @@ SIGNATURES = {
                                         C.POINTER(C.c_size_t)]),
     "gf_attn_fwd_strategy": (C.c_int, [_vp, C.POINTER(AttnDesc), C.c_int32, _vp, _vp, _vp, _vp,
                                        _vp, _vp, _vp, C.c_size_t, _vp]),
+    "gf_time_fwd_strategy": (C.c_int, [_vp, C.POINTER(AttnDesc), C.c_int32, _vp, _vp, _vp, _vp,
+                                       _vp, C.c_int32, C.POINTER(C.c_float), _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp]),
     "gf_attn_bwd_rows": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(256) softmax_rows(const FwdArgs<T> a, const T*
 // ---- feature-parallel fused baseline (the pre-DF-GNN fused kernel) ---------
 // Warp per destination row in id order; lane owns features f = lane + 32 i.
 // Per edge every lane rebuilds the score of ITS feature's head — for dot
-// scores by summing the head's D partial products from shared memory — so
-// each of the D lanes of a head repeats the row's softmax work.  Two
+// scores by a shuffle reduction of the head's D partial products (shared
+// memory for D that neither divides nor is a multiple of 32) — so each of the
+// D lanes of a head repeats the row's softmax work.  Two
 // sweeps over the row (max, then exp/sum/aggregate).
 template <typename T, int VAR, int NF>
 __global__ void __launch_bounds__(128) fwd_feature_parallel(const FwdArgs<T> a) {
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(128) fwd_feature_parallel(const FwdArgs<T> a) 
     }
     __syncwarp();
   }
+  const bool shuf = (32 % a.D == 0) || (a.D % 32 == 0);
   // score of every owned feature's head for source u (all lanes participate)
   auto scores = [&](int u, T (&s)[NF]) {
     if constexpr (VAR == GF_ADD) {
@@ -179,7 +181,38 @@ __global__ void __launch_bounds__(128) fwd_feature_parallel(const FwdArgs<T> a) 
       for (int i = 0; i < NF; ++i)
         s[i] = in[i] ? lrelu(__ldg(a.Q + static_cast<size_t>(u) * a.H + hf[i]) + erf[i], a.slope)
                      : T(0);
-    } else {
+    } else if (shuf) {
+      // head sums by warp shuffles: within aligned groups of D lanes (D | 32)
+      // or over the whole warp after summing the D/32 features a lane holds
+      T pq[NF], qq2[NF];
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        const T q = in[i] ? __ldg(a.Q + static_cast<size_t>(u) * a.F + lane + 32 * i) : T(0);
+        pq[i] = q * kf[i];
+        qq2[i] = q * q;
+      }
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        T d = T(0), qq = T(0);
+        if (a.D <= 32) {
+          d = pq[i], qq = qq2[i];
+          for (int o = 1; o < a.D; o <<= 1) {
+            d += __shfl_xor_sync(kFull, d, o);
+            qq += __shfl_xor_sync(kFull, qq, o);
+          }
+        } else {
+          const int G = a.D / 32;  // features of one head held by this lane
+#pragma unroll
+          for (int j = 0; j < NF; ++j)
+            if (j / G == i / G) d += pq[j], qq += qq2[j];
+          for (int o = 1; o < 32; o <<= 1) {
+            d += __shfl_xor_sync(kFull, d, o);
+            qq += __shfl_xor_sync(kFull, qq, o);
+          }
+        }
+        s[i] = a.l2 ? a.scale * d * (inv_norm(qq) * rkf[i]) : a.scale * d;
+      }
+    } else {  // D neither divides nor is a multiple of 32: partials via shared memory
 #pragma unroll
       for (int i = 0; i < NF; ++i) {
         const T q = in[i] ? __ldg(a.Q + static_cast<size_t>(u) * a.F + lane + 32 * i) : T(0);

@@ -204,6 +204,40 @@ extern "C" int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int3
   return rc;
 }
 
+extern "C" int gf_time_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strategy,
+                                    const void* Q, const void* K, const void* V, void* O,
+                                    void* stats, int32_t reps, float* ms_out, void* stream) {
+  if (!ms_out || reps < 1) {
+    gfb::set_error("gf_time_fwd_strategy: invalid arguments");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  size_t need = 0;
+  if (int rc = gf_attn_fwd_workspace(g, desc, strategy, 0, &need)) return rc;
+  void* ws = nullptr;
+  if (need) GF_CHECK_CUDA(cudaMallocAsync(&ws, need, s));
+  cudaEvent_t a = nullptr, b = nullptr;
+  int rc = GF_OK;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+    gfb::set_error("gf_time_fwd_strategy: cudaEventCreate failed");
+    rc = GF_ERR_CUDA;
+  }
+  if (!rc) rc = gf_attn_fwd_strategy(g, desc, strategy, Q, K, V, O, stats, nullptr, ws, need, stream);
+  if (!rc && cudaEventRecord(a, s) != cudaSuccess) rc = GF_ERR_CUDA;
+  for (int i = 0; i < reps && !rc; ++i)
+    rc = gf_attn_fwd_strategy(g, desc, strategy, Q, K, V, O, stats, nullptr, ws, need, stream);
+  if (!rc && cudaEventRecord(b, s) != cudaSuccess) rc = GF_ERR_CUDA;
+  if (!rc && cudaEventSynchronize(b) != cudaSuccess) rc = GF_ERR_CUDA;
+  float ms = 0.f;
+  if (!rc && cudaEventElapsedTime(&ms, a, b) != cudaSuccess) rc = GF_ERR_CUDA;
+  if (rc == GF_ERR_CUDA) gfb::set_error("gf_time_fwd_strategy: CUDA event failure");
+  *ms_out = ms / reps;
+  if (a) cudaEventDestroy(a);
+  if (b) cudaEventDestroy(b);
+  if (ws) cudaFreeAsync(ws, s);
+  return rc;
+}
+
 extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                            const void* V, const void* O, void* stats, const void* dO, void* dQ,
                            void* dK, void* dV, void* stream) {

@@ -156,6 +156,31 @@ void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>
   }
 }
 
+/// Measured GPU time (ms) of `mode`'s forward kernels on device-resident
+/// copies of Q, K, V (the bench harness's measured column).
+template <typename T>
+double device_forward_ms(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>& Q,
+                         const DenseMatrix<T>& K, const DenseMatrix<T>& V, const SddmmKind& kind,
+                         Strategy mode, int reps) {
+  validate_inputs(g, Q, K, V, kind);
+  gf_graph_t dg = device_graph(g, plan);
+  const gf_attn_desc desc = make_desc<T>(kind, V.cols);
+  DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), dv = DevBuf::from(V.data);
+  DevBuf dO(sizeof(T) * static_cast<size_t>(g.num_nodes * V.cols)),
+      dl(sizeof(T) * static_cast<size_t>(4 * g.num_nodes));
+  float ms = 0.f;
+  GFH_CALL(gf_time_fwd_strategy(dg, &desc, strategy_code(mode), dq.p, dk.p, dv.p, dO.p, dl.p,
+                                reps, &ms, nullptr));
+  return ms;
+}
+template double device_forward_ms<float>(const Graph&, const FusionPlan&, const DenseMatrix<float>&,
+                                         const DenseMatrix<float>&, const DenseMatrix<float>&,
+                                         const SddmmKind&, Strategy, int);
+template double device_forward_ms<double>(const Graph&, const FusionPlan&,
+                                          const DenseMatrix<double>&, const DenseMatrix<double>&,
+                                          const DenseMatrix<double>&, const SddmmKind&, Strategy,
+                                          int);
+
 template <typename T>
 ForwardResult<T> run_mode(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
                           const DenseMatrix<T>& V, const SddmmKind& kind, const FusionPlan& plan,

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "graphfuse/autograd.hpp"
+#include "graphfuse/bench.hpp"
 #include "graphfuse/engine.hpp"
 #include "graphfuse/models.hpp"
 
@@ -222,12 +223,87 @@ static void layer_cases() {
   }
 }
 
+// test_models.cpp:154-233 (benchmark runner, auto strategy, config parsing)
+static void bench_cases() {
+  BenchConfig cfg;
+  cfg.model = "gt";
+  cfg.nodes = 119;
+  cfg.avg_degree = 12.0;
+  cfg.batch_count = 4;
+  cfg.dim = 32;
+  cfg.seed = 3;
+  cfg.strategies = {"auto", "unfused", "smmf", "pmf", "baseline"};
+  cfg.peak_bw = 1.0e12;
+  {
+    BenchConfig bad = cfg;
+    bad.peak_bw = 0.0;
+    bool threw = false;
+    try {
+      run_benchmark(bad);
+    } catch (const BenchError&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
+  auto report = run_benchmark(cfg);
+  EXPECT(report.num_nodes == 119 * 4);
+  EXPECT(report.selected_strategy == "smmf");
+  EXPECT(report.rows.size() == 4);
+  EXPECT(report.rows[0].mode == "unfused");
+  auto again = run_benchmark(cfg);
+  for (size_t i = 0; i < report.rows.size() && i < again.rows.size(); ++i) {
+    EXPECT(report.rows[i].mode == again.rows[i].mode);
+    EXPECT(report.rows[i].counters.same_model(again.rows[i].counters));
+    EXPECT(report.rows[i].device_ms > 0);  // every mode ran its own kernels
+  }
+  const std::string csv = report_csv(report);
+  EXPECT(csv.rfind("mode,elapsed_ns,kernel_launches,global_bytes_read,"
+                   "global_bytes_written,shared_bytes,memory_transactions,"
+                   "softmax_scalar_ops,max_group_load,mean_group_load,"
+                   "speedup_vs_unfused,bandwidth_utilization\n",
+                   0) == 0);
+  EXPECT(std::count(csv.begin(), csv.end(), '\n') == static_cast<long>(1 + report.rows.size()));
+  EXPECT(report_markdown(report).find("| mode |") != std::string::npos);
+  const std::string dcsv = report_csv_device(report);
+  EXPECT(dcsv.find(",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization\n") !=
+         std::string::npos);
+
+  BenchConfig g = cfg;  // auto never picks PMF for additive attention
+  g.model = "gat";
+  g.nodes = 300;
+  g.avg_degree = 2.0;
+  g.hub_degree = 260;
+  g.dim = 4;
+  g.seed = 5;
+  g.batch_count = 1;
+  g.strategies = {"auto"};
+  EXPECT(run_benchmark(g).selected_strategy != "pmf");
+
+  BenchConfig p = config_from_json(R"({
+    "model": "agnn", "nodes": 77, "avg_degree": 3.5, "dim": 16,
+    "dtype": "f64", "seed": 9, "strategies": ["smmf", "unfused"],
+    "deterministic": true, "peak_bw": 2.5e11
+  })");
+  EXPECT(p.model == "agnn" && p.nodes == 77 && p.avg_degree == 3.5 && p.dim == 16);
+  EXPECT(p.dtype == "f64" && p.seed == 9 && p.strategies.size() == 2 && p.peak_bw == 2.5e11);
+  bool bad_json = false;
+  try {
+    config_from_json("{not json");
+  } catch (const BenchError&) {
+    bad_json = true;
+  }
+  EXPECT(bad_json);
+  auto r64 = run_benchmark(p);  // f64 agreement gate at 1e-11
+  EXPECT(r64.rows.size() == 2);
+}
+
 int main() {
   modes_match_dense();
   launches_and_traffic();
   feasibility_error();
   backward_cases();
   layer_cases();
+  bench_cases();
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

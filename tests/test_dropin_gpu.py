@@ -152,3 +152,44 @@ def test_smmf_infeasible_plan_raises(cuda):
     x = np.zeros((20000, 1))
     with pytest.raises(RuntimeError, match="block 0.*requires"):
         gf.forward(g, x, x, x)  # default strategy smmf, 48 KiB budget
+
+
+# The reference's two shipped bench scenarios (proj/configs/hub.json and
+# pattern.json), restated as dicts.
+BENCH_CONFIGS = {
+    "hub": {"model": "gt", "nodes": 100, "avg_degree": 4.0, "hub_degree": 90, "dim": 64,
+            "dtype": "f32", "seed": 7, "strategies": ["auto", "smmf", "pmf", "baseline"],
+            "deterministic": True, "peak_bw": 1.0e12},
+    "pattern": {"model": "gt", "nodes": 119, "avg_degree": 51.0, "batch_count": 8, "dim": 128,
+                "dtype": "f32", "seed": 13, "strategies": ["auto", "pmf", "baseline"],
+                "deterministic": True, "peak_bw": 1.0e12},
+}
+CSV_HEADER = ("mode,elapsed_ns,kernel_launches,global_bytes_read,global_bytes_written,"
+              "shared_bytes,memory_transactions,softmax_scalar_ops,max_group_load,"
+              "mean_group_load,speedup_vs_unfused,bandwidth_utilization")
+
+
+@pytest.mark.parametrize("name", sorted(BENCH_CONFIGS))
+def test_run_benchmark_json(cuda, name):
+    """Bench harness parity: same CSV columns and rows as the reference, the
+    unfused row first, the agreement gate passed (every mode runs its own
+    kernels), modelled counters identical across runs; the device CSV adds the
+    measured GPU time per mode."""
+    import json
+
+    text = json.dumps(BENCH_CONFIGS[name])
+    csv = _core.run_benchmark_json(text)
+    lines = csv.strip().split("\n")
+    assert lines[0] == CSV_HEADER
+    modes = [ln.split(",")[0] for ln in lines[1:]]
+    assert modes[0] == "unfused" and len(set(modes)) == len(modes)
+    cfg = BENCH_CONFIGS[name]
+    assert set(modes) >= {s for s in cfg["strategies"] if s != "auto"}
+    again = _core.run_benchmark_json(text).strip().split("\n")
+    strip = lambda ln: ln.split(",")[2:10]  # noqa: E731  counters, not timings
+    assert [strip(a) for a in lines[1:]] == [strip(b) for b in again[1:]]
+    dcsv, md = _core.run_benchmark_json_device(text)
+    dl = dcsv.strip().split("\n")
+    assert dl[0] == CSV_HEADER + ",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization"
+    assert all(float(r.split(",")[12]) > 0 for r in dl[1:])
+    assert "| mode |" in md

@@ -158,3 +158,19 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         gf.forward(g, x, x, x)
     with pytest.raises(RuntimeError, match="no sm_100 device"):
         gf.backward(g, x, x, x, x)
+
+
+def test_bench_config_errors_before_any_device_work():
+    """run_benchmark_json (module.cpp:151-154) validates the config first: a
+    missing peak_bw and malformed JSON raise BenchError -> RuntimeError
+    (bench.cpp:51-53, 153-159), on a host with or without a GPU."""
+    import json
+
+    with pytest.raises(RuntimeError, match="peak_bw"):
+        _core.run_benchmark_json(json.dumps({"model": "gt", "nodes": 50, "peak_bw": 0}))
+    with pytest.raises(RuntimeError, match="bad config"):
+        _core.run_benchmark_json("{ not json")
+    with pytest.raises(RuntimeError, match="bad config"):
+        _core.run_benchmark_json(json.dumps({"nodes": "many", "peak_bw": 1e12}))
+    with pytest.raises(RuntimeError, match="unknown dtype"):
+        _core.run_benchmark_json(json.dumps({"dtype": "f16", "peak_bw": 1e12}))
