@@ -438,6 +438,40 @@ def strategy_ablation(dg, spec, Q, K, V, O, stats, stream, flush, steps=5):
     return out
 
 
+def backward_ablation(dg, spec, Q, K, V, O, stats, dO, stream, flush, steps=5):
+    """Backward time: this design's fused recompute (pass A + pass B, nothing
+    E x H in HBM) vs the reference's unfused 5-launch schedule (dP + dV,
+    softmax backward, dQ + dK over a stored P, autograd.hpp:158-170)."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    out = {}
+    try:
+        O, stats, P = fused.attn_forward(dg, spec, Q, K, V, want_p=True, stream=stream)
+        runs = {"fused": lambda: fused.attn_backward(dg, spec, Q, K, V, O, stats, dO, stream=stream),
+                "unfused": lambda: fused.attn_backward_unfused(dg, spec, Q, K, V, P, dO,
+                                                               stream=stream)}
+        for name, fn in runs.items():
+            for _ in range(2):
+                fn()
+            ms = []
+            for _ in range(steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+            out[name] = round(statistics.mean(ms), 4)
+        del P
+    except Exception as ex:  # reported, never silently replaced
+        out["error"] = str(ex)
+    torch.cuda.synchronize()
+    return out
+
+
 def run_ours(args, rank, world):
     import numpy as np
     import torch
@@ -617,9 +651,10 @@ def run_ours(args, rank, world):
     layer_out = None
     if not sharded and not args.no_layer:
         layer_out = layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush)
-    ablation = None
+    ablation = bwd_ablation = None
     if not sharded and not args.no_ablation:
         ablation = strategy_ablation(dg, spec, Q, K, V, O, stats, stream, flush)
+        bwd_ablation = backward_ablation(dg, spec, Q, K, V, O, stats, dO, stream, flush)
 
     # ---- roofline of the dominant kernel
     means = {"fwd": statistics.mean(k_fwd), "bwd_rows": statistics.mean(k_ra),
@@ -678,6 +713,7 @@ def run_ours(args, rank, world):
                     "d2h_bytes_per_step": d2h},
             "layer": layer_out,
             "fwd_strategy_ms": ablation,
+            "bwd_strategy_ms": bwd_ablation,
             "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
         }

@@ -166,6 +166,41 @@ int gf_time_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int32_t strateg
                          const void* K, const void* V, void* O, void* stats, int32_t reps,
                          float* ms_out, void* stream);
 
+/* ---- single-step operators (the unfused schedule's building blocks) ----
+ * E x H edge tensors are CSR-ordered, head-minor ([e][h]).  Each call is
+ * one kernel (two for spmm_backward / sddmm_backward) and moves its E x H
+ * operands through HBM, as the reference's unfused counters model.
+ * Ops that visit the CSC view need an unsharded graph. */
+/* sddmm (kernels.hpp:18-47, 106-117): S[e,h] = scale <Q[src], K[dst]> (dot;
+ * l2: on L2-normalised rows) or LeakyReLU(el[src] + er[dst]) (add). */
+int gf_sddmm(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K, void* S,
+             void* stream);
+/* edge_softmax (kernels.hpp:65-82): per destination row and head. */
+int gf_edge_softmax(gf_graph_t g, int32_t dtype, int32_t heads, const void* S, void* P,
+                    void* stream);
+/* spmm (kernels.hpp:85-102): O[v] = sum_{e in row v} P[e] V[src e] per head. */
+int gf_spmm(gf_graph_t g, int32_t dtype, int32_t heads, int32_t head_dim, const void* P,
+            const void* V, void* O, void* stream);
+/* l2_normalize_rows (kernels.hpp:50-61) per head segment (x / max(||x||,
+ * eps), eps > 0) and its backward (autograd.hpp:76-95).  X, Y, dY, dX:
+ * n x (heads*head_dim). */
+int gf_l2_normalize_rows(int32_t dtype, int64_t n, int32_t heads, int32_t head_dim, const void* X,
+                         void* Y, double eps, void* stream);
+int gf_l2_normalize_backward(int32_t dtype, int64_t n, int32_t heads, int32_t head_dim,
+                             const void* X, const void* dY, void* dX, double eps, void* stream);
+/* spmm_backward (autograd.hpp:33-58): dP[e] = <dO[dst], V[src]>,
+ * dV[u] = sum over u's out-edges of P[e] dO[dst]. */
+int gf_spmm_backward(gf_graph_t g, int32_t dtype, int32_t heads, int32_t head_dim, const void* P,
+                     const void* V, const void* dO, void* dP, void* dV, void* stream);
+/* softmax_backward (autograd.hpp:62-73): dS = P (dP - sum_row P dP). */
+int gf_softmax_backward(gf_graph_t g, int32_t dtype, int32_t heads, const void* P, const void* dP,
+                        void* dS, void* stream);
+/* sddmm_backward (autograd.hpp:102-154): dot -> dQ (out-edges, K[dst]) and
+ * dK (in-edges, Q[src]), through the L2 normalisation when desc->l2; add ->
+ * del, der (N x H) with the LeakyReLU derivative (kink takes the slope). */
+int gf_sddmm_backward(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
+                      const void* dS, void* dQ, void* dK, void* stream);
+
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
  * Pass A over CSR rows (dK or der, and delta into stats), pass B over CSC
  * columns (dQ or del, dV).  Attention is recomputed from the stats records;

@@ -285,20 +285,69 @@ ForwardResult<T> run_strategy(const Graph& g, const DenseMatrix<T>& Q, const Den
   return detail::run_mode(g, Q, K, V, kind, plan, plan.strategy);
 }
 
+// ----------------------------------------------------------- kernels.hpp --
+// Single-step operators (kernels.hpp:18-117), each one device op
+// (gf_sddmm / gf_edge_softmax / gf_spmm / gf_l2_normalize_rows).  The dense
+// masked test oracle dense_oracle_forward (kernels.hpp:122-166) is test
+// infrastructure and lives with the other CPU checkers under oracle/.
+template <typename T>
+EdgeScalars<T> sddmm_dot(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                         T scale);
+template <typename T>
+EdgeScalars<T> sddmm_add(const Graph& g, const DenseMatrix<T>& el, const DenseMatrix<T>& er,
+                         T leaky_slope);
+template <typename T>
+DenseMatrix<T> l2_normalize_rows(const DenseMatrix<T>& X, T eps);
+template <typename T>
+EdgeScalars<T> edge_softmax(const Graph& g, const EdgeScalars<T>& s);
+template <typename T>
+DenseMatrix<T> spmm(const Graph& g, const EdgeScalars<T>& p, const DenseMatrix<T>& V);
+template <typename T>
+EdgeScalars<T> sddmm(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                     const SddmmKind& kind);
+
 // --------------------------------------------------------------- autograd --
 template <typename T>
 struct GradBundle {
   DenseMatrix<T> dQ, dK, dV;
-  /// Edge gradients are never materialised by the B200 path (recompute
-  /// design); these stay empty.
+  /// Edge gradients: filled by the unfused schedule (unfused_backward, and
+  /// fused_backward's infeasible-plan fallback); the fused recompute path
+  /// never materialises E-sized tensors and leaves them empty.
   EdgeScalars<T> dS, dP;
 };
+
+/// Backward single steps (autograd.hpp:33-154), each a device op.
+template <typename T>
+std::pair<EdgeScalars<T>, DenseMatrix<T>> spmm_backward(const Graph& g, const EdgeScalars<T>& P,
+                                                        const DenseMatrix<T>& V,
+                                                        const DenseMatrix<T>& dO);
+template <typename T>
+EdgeScalars<T> softmax_backward(const Graph& g, const EdgeScalars<T>& P, const EdgeScalars<T>& dP);
+template <typename T>
+DenseMatrix<T> l2_normalize_backward(const DenseMatrix<T>& X, const DenseMatrix<T>& dY, T eps);
+template <typename T>
+std::pair<DenseMatrix<T>, DenseMatrix<T>> sddmm_backward(const Graph& g, const DenseMatrix<T>& Q,
+                                                         const DenseMatrix<T>& K,
+                                                         const EdgeScalars<T>& dS,
+                                                         const SddmmKind& kind);
 
 template <typename T>
 struct BackwardResult {
   GradBundle<T> grads;
   ExecCounters counters;
 };
+
+namespace detail {
+/// The unfused composition spmm_backward -> softmax_backward ->
+/// sddmm_backward on the device (autograd.hpp:158-170), 5 launches, edge
+/// gradients returned in dP / dS.  Uses ctx.P when it holds E values.
+template <typename T>
+GradBundle<T> backward_values(const Graph& g, const ForwardContext<T>& ctx,
+                              const DenseMatrix<T>& dO);
+template <typename T>
+ExecCounters backward_counter_model(const Graph& g, const ForwardContext<T>& ctx,
+                                    std::int64_t launches);
+}  // namespace detail
 
 template <typename T>
 BackwardResult<T> unfused_backward(const Graph& g, const ForwardContext<T>& ctx,

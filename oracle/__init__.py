@@ -63,6 +63,9 @@ def lib():
             b.argtypes = [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int,
                           C.c_int, C.c_int, C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp,
                           _vp, _vp]
+            b2 = getattr(_ora, "gfo_backward2_" + sfx)
+            b2.restype = C.c_int
+            b2.argtypes = b.argtypes + [_vp, _vp]
     return _ora
 
 
@@ -193,19 +196,25 @@ def forward(g: CSR, Q, K, V, H, D, variant="dot", l2=False, scale=1.0, slope=0.2
     return out[0] if len(out) == 1 else tuple(out)
 
 
-def backward(g: CSR, Q, K, V, dO, H, D, variant="dot", l2=False, scale=1.0, slope=0.2):
-    """Multi-head backward restatement (autograd.hpp:158-170 per head)."""
+def backward(g: CSR, Q, K, V, dO, H, D, variant="dot", l2=False, scale=1.0, slope=0.2,
+             want_edge_grads=False):
+    """Multi-head backward restatement (autograd.hpp:158-170 per head).
+    Returns (dQ, dK, dV), plus (dP, dS) (E x H, CSR order) on request."""
     dt = V.dtype
     var = 1 if variant == "add" else 0
     w = H if var == 1 else H * D
     dQ = np.zeros((g.n, w), dt)
     dK = np.zeros((g.n, w), dt)
     dV = np.zeros((g.n, H * D), dt)
-    f = getattr(lib(), "gfo_backward_" + _sfx(dt))
+    dP = np.zeros((max(g.e, 1), H), dt) if want_edge_grads else None
+    dS = np.zeros((max(g.e, 1), H), dt) if want_edge_grads else None
+    f = getattr(lib(), "gfo_backward2_" + _sfx(dt))
     f(g.n, g.e, _ptr(g.row_ptr), _ptr(g.col), _ptr(g.csc_ptr), _ptr(g.csc_row), _ptr(g.csc_perm),
       H, D, var, int(l2), scale, slope, _ptr(np.ascontiguousarray(Q, dt)),
       _ptr(np.ascontiguousarray(K, dt)), _ptr(np.ascontiguousarray(V, dt)),
-      _ptr(np.ascontiguousarray(dO, dt)), _ptr(dQ), _ptr(dK), _ptr(dV))
+      _ptr(np.ascontiguousarray(dO, dt)), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dP), _ptr(dS))
+    if want_edge_grads:
+        return dQ, dK, dV, dP[: g.e], dS[: g.e]
     return dQ, dK, dV
 
 

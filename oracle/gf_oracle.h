@@ -58,6 +58,18 @@ int gfo_backward_f64(int64_t n, int64_t e, const int64_t* row_ptr, const int64_t
                      const double* Q, const double* K, const double* V, const double* dO,
                      double* dQ, double* dK, double* dV);
 
+/* Same plus the edge gradients dP and dS (E x H, CSR order; nullable). */
+int gfo_backward2_f32(int64_t n, int64_t e, const int64_t* row_ptr, const int64_t* col,
+                      const int64_t* csc_ptr, const int64_t* csc_row, const int64_t* csc_perm,
+                      int H, int D, int variant, int l2, double scale, double slope,
+                      const float* Q, const float* K, const float* V, const float* dO, float* dQ,
+                      float* dK, float* dV, float* dP, float* dS);
+int gfo_backward2_f64(int64_t n, int64_t e, const int64_t* row_ptr, const int64_t* col,
+                      const int64_t* csc_ptr, const int64_t* csc_row, const int64_t* csc_perm,
+                      int H, int D, int variant, int l2, double scale, double slope,
+                      const double* Q, const double* K, const double* V, const double* dO,
+                      double* dQ, double* dK, double* dV, double* dP, double* dS);
+
 #ifdef __cplusplus
 }
 #endif

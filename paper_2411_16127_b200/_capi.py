@@ -63,6 +63,17 @@ SIGNATURES = {
                                        _vp, _vp, _vp, C.c_size_t, _vp]),
     "gf_time_fwd_strategy": (C.c_int, [_vp, C.POINTER(AttnDesc), C.c_int32, _vp, _vp, _vp, _vp,
                                        _vp, C.c_int32, C.POINTER(C.c_float), _vp]),
+    "gf_sddmm": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp]),
+    "gf_edge_softmax": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp]),
+    "gf_spmm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
+    "gf_l2_normalize_rows": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, _vp, _vp,
+                                       C.c_double, _vp]),
+    "gf_l2_normalize_backward": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, _vp, _vp,
+                                           _vp, C.c_double, _vp]),
+    "gf_spmm_backward": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp,
+                                   _vp]),
+    "gf_softmax_backward": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
+    "gf_sddmm_backward": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp]),
     "gf_attn_bwd_rows": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,

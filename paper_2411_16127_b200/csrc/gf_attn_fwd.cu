@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
   // Destination-side operands stay in registers for the whole row.
   T kv[NE];
   T erv = T(0), rk = T(1);
-  if constexpr (MODE == 2) {
+  if constexpr (MODE >= 2) {
     // probabilities given: no destination-side score operands
   } else if constexpr (VAR == GF_DOT) {
     if (MODE == 0 || a.l2) {
@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
           ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
-        if constexpr (MODE != 0) {
+        if constexpr (MODE == 3) {
+          s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
+        } else if constexpr (MODE != 0) {
           s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(base + j) * a.H) : T(0);
         } else if constexpr (VAR == GF_DOT) {
 #pragma unroll
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
           s[t] = ld_node(Qb + uu * qs);
         }
       }
-      if constexpr (MODE == 2) {
+      if constexpr (MODE >= 2) {
 #pragma unroll
         for (int t = 0; t < U; ++t) {
 #pragma unroll
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
     for (int i = 0; i < NE; ++i) acc2[i] = __shfl_xor_sync(kFull, acc[i], o);
     const T m2 = __shfl_xor_sync(kFull, m, o);
     const T l2 = __shfl_xor_sync(kFull, l, o);
-    if constexpr (MODE == 2) {
+    if constexpr (MODE >= 2) {
 #pragma unroll
       for (int i = 0; i < NE; ++i) acc[i] += acc2[i];
     } else {
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
         T acc2[NE];
 #pragma unroll
         for (int i = 0; i < NE; ++i) acc2[i] = d[2 + i];
-        if constexpr (MODE == 2) {
+        if constexpr (MODE >= 2) {
 #pragma unroll
           for (int i = 0; i < NE; ++i) acc[i] += acc2[i];
         } else {
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
   }
 
   if (sub == 0) {
-    const T r = MODE == 2 ? T(1) : (l == T(0) ? T(0) : T(1) / l);
+    const T r = MODE >= 2 ? a.scale : (l == T(0) ? T(0) : T(1) / l);
     T o[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) o[i] = acc[i] * r;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       st_chunk<T, CB>(orow + k * CW, *reinterpret_cast<T(*)[CW]>(o + k * CW));
-    if (MODE != 2 && c % a.LPH == 0) {
+    if (MODE < 2 && c % a.LPH == 0) {
       T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + h);
       rec[0] = l == T(0) ? ninf<T>() : m;
       rec[1] = l == T(0) ? T(0) : lg2(l);
@@ -255,14 +257,14 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   const int v = __ldg(a.order + slot);
   const int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
   for (int f = lane; f < a.F; f += 32) {
-    if constexpr (VAR == GF_DOT) kvs[f] = __ldg(a.K + static_cast<size_t>(v) * a.F + f);
+    if constexpr (VAR == GF_DOT && MODE < 2) kvs[f] = __ldg(a.K + static_cast<size_t>(v) * a.F + f);
     acc[f] = T(0);
   }
   __syncwarp();
-  T erh, rkh;
-  generic_row_setup<T, VAR>(a, v, lane, VAR == GF_DOT ? kvs : nullptr, erh, rkh);
+  T erh = T(0), rkh = T(1);
+  if (MODE < 2) generic_row_setup<T, VAR>(a, v, lane, VAR == GF_DOT ? kvs : nullptr, erh, rkh);
   T m = ninf<T>(), l = T(0);
-  if (MODE != 2) {
+  if (MODE < 2) {
     for (int i = eb; i < ee; ++i) {
       if (lane < a.H) {
         const T s = MODE == 1 ? ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane)
@@ -275,7 +277,9 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
     const int u = __ldg(a.idx + i);
     if (lane < a.H) {
       T p;
-      if constexpr (MODE == 2)
+      if constexpr (MODE == 3)
+        p = ld_edge(a.ES + static_cast<size_t>(__ldg(a.eperm + i)) * a.H + lane);
+      else if constexpr (MODE == 2)
         p = ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane);
       else if constexpr (MODE == 1)
         p = expd(ld_edge(a.ES + static_cast<size_t>(i) * a.H + lane) - m);
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
       acc[f] += ph[f / a.D] * __ldg(a.V + static_cast<size_t>(u) * a.F + f);
     __syncwarp();
   }
-  if (MODE == 2) {
+  if (MODE >= 2) {
     if (lane < a.H) lh[lane] = T(1);
   } else if (lane < a.H) {
     lh[lane] = l;
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
   for (int f = lane; f < a.F; f += 32) {
     const T lv = lh[f / a.D];
     a.O[static_cast<size_t>(v) * a.F + f] =
-        MODE == 2 ? acc[f] : (lv == T(0) ? T(0) : acc[f] / lv);
+        MODE >= 2 ? acc[f] * a.scale : (lv == T(0) ? T(0) : acc[f] / lv);
   }
 }
 
@@ -326,8 +330,10 @@ __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __re
 
 template <typename T, int CB, int LPE, int CPL>
 int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cudaStream_t s) {
-  if (mode == 2)  // probabilities given: the score variant is irrelevant
+  if (mode == 2)  // edge weights given: the score variant is irrelevant
     fwd_fast<T, CB, LPE, CPL, GF_ADD, 2><<<blocks, 256, 0, s>>>(a);
+  else if (mode == 3)
+    fwd_fast<T, CB, LPE, CPL, GF_ADD, 3><<<blocks, 256, 0, s>>>(a);
   else if (mode == 1 && variant == GF_DOT)
     fwd_fast<T, CB, LPE, CPL, GF_DOT, 1><<<blocks, 256, 0, s>>>(a);
   else if (mode == 1)
@@ -392,7 +398,7 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
   const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
   const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
                   aligned(a.stats, 32) &&
-                  (mode == 2 || variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
+                  (mode >= 2 || variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
   if (al) {
     a.LPH = fs.lph;
     const int warp_rows = a.n - a.n_cta;
@@ -430,6 +436,7 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     return GF_ERR_UNSUPPORTED;
   }
   if (mode == 2) return launch_generic<T, GF_ADD, 2>(a, smem, s);
+  if (mode == 3) return launch_generic<T, GF_ADD, 3>(a, smem, s);
   if (mode == 1)
     return variant == GF_DOT ? launch_generic<T, GF_DOT, 1>(a, smem, s)
                              : launch_generic<T, GF_ADD, 1>(a, smem, s);

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) softmax_rows(const FwdArgs<T> a, const T*
       for (size_t i = lane; i < len; i += H) P[base + i] = expd(ld_edge(S + base + i) - m) * r;
     }
   }
-  if (lane < H) {
+  if (a.stats && lane < H) {
     T erh, rkh;
     generic_row_setup<T, VAR>(a, v, lane, nullptr, erh, rkh);
     T* rec = a.stats + 4 * (static_cast<size_t>(v) * H + h);
@@ -295,6 +295,12 @@ int launch_fp(const FwdArgs<T>& a, cudaStream_t s) {
   return GF_OK;
 }
 
+int grid_1d(int64_t work) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 16, (work + 255) / 256)));
+}
+
+}  // namespace
+
 int ensure_coo_dst(DevGraph& g, cudaStream_t s) {
   if (g.coo_dst || g.e == 0) return GF_OK;
   GF_CHECK_CUDA(cudaMalloc(&g.coo_dst, sizeof(int32_t) * g.e));
@@ -304,11 +310,43 @@ int ensure_coo_dst(DevGraph& g, cudaStream_t s) {
   return GF_OK;
 }
 
-int grid_1d(int64_t work) {
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 16, (work + 255) / 256)));
+template <typename T>
+int launch_sddmm_edges(DevGraph& g, const FwdArgs<T>& a, int variant, T* S, cudaStream_t s) {
+  if (g.e == 0) return GF_OK;
+  if (int rc = ensure_coo_dst(g, s)) return rc;
+  const int64_t eh = static_cast<int64_t>(g.e) * a.H;
+  if (variant == GF_DOT)
+    sddmm_edges<T, GF_DOT><<<grid_1d(eh), 256, 0, s>>>(a, g.coo_dst, g.e, S);
+  else
+    sddmm_edges<T, GF_ADD><<<grid_1d(eh), 256, 0, s>>>(a, g.coo_dst, g.e, S);
+  GF_CHECK_LAUNCH("sddmm_edges");
+  return GF_OK;
 }
 
-}  // namespace
+template <typename T>
+int launch_softmax_rows(const DevGraph& g, const FwdArgs<T>& a, int variant, const T* S, T* P,
+                        cudaStream_t s) {
+  if (a.n == 0) return GF_OK;
+  if (a.H > 32) {
+    set_error("edge softmax: heads <= 32 supported");
+    return GF_ERR_UNSUPPORTED;
+  }
+  const int blocks = static_cast<int>((static_cast<int64_t>(a.n) * 32 + 255) / 256);
+  if (variant == GF_DOT)
+    softmax_rows<T, GF_DOT><<<blocks, 256, 0, s>>>(a, S, P);
+  else
+    softmax_rows<T, GF_ADD><<<blocks, 256, 0, s>>>(a, S, P);
+  GF_CHECK_LAUNCH("softmax_rows");
+  return GF_OK;
+}
+
+template int launch_sddmm_edges<float>(DevGraph&, const FwdArgs<float>&, int, float*, cudaStream_t);
+template int launch_sddmm_edges<double>(DevGraph&, const FwdArgs<double>&, int, double*,
+                                        cudaStream_t);
+template int launch_softmax_rows<float>(const DevGraph&, const FwdArgs<float>&, int, const float*,
+                                        float*, cudaStream_t);
+template int launch_softmax_rows<double>(const DevGraph&, const FwdArgs<double>&, int,
+                                         const double*, double*, cudaStream_t);
 
 size_t strategy_workspace_bytes(const DevGraph& g, int heads, int elem, int strategy, bool have_p) {
   const size_t eh = static_cast<size_t>(g.e) * heads * elem;
@@ -328,33 +366,18 @@ int launch_fwd_strategy(DevGraph& g, const FwdArgs<T>& a, int variant, int strat
       return P ? launch_materialize_p<T>(g, a, variant, P, s) : GF_OK;
     case GF_STRAT_PMF:
     case GF_STRAT_UNFUSED: {
-      if (int rc = ensure_coo_dst(g, s)) return rc;
       T* S = ws;
-      if (g.e > 0) {
-        if (variant == GF_DOT)
-          sddmm_edges<T, GF_DOT><<<grid_1d(eh), 256, 0, s>>>(a, g.coo_dst, g.e, S);
-        else
-          sddmm_edges<T, GF_ADD><<<grid_1d(eh), 256, 0, s>>>(a, g.coo_dst, g.e, S);
-        GF_CHECK_LAUNCH("sddmm_edges");
-      }
+      if (int rc = launch_sddmm_edges<T>(g, a, variant, S, s)) return rc;
       FwdArgs<T> b = a;
       if (strategy == GF_STRAT_PMF) {
         b.ES = S;
         if (int rc = launch_fwd_mode<T>(g, b, variant, 1, s)) return rc;
         return P ? launch_materialize_p<T>(g, a, variant, P, s) : GF_OK;
       }
-      if (a.H > 32) {
-        set_error("gf_attn_fwd_strategy: the unfused softmax kernel supports heads <= 32");
-        return GF_ERR_UNSUPPORTED;
-      }
       T* Pw = P ? P : ws + eh;
-      const int blocks = static_cast<int>((static_cast<int64_t>(a.n) * 32 + 255) / 256);
-      if (variant == GF_DOT)
-        softmax_rows<T, GF_DOT><<<blocks, 256, 0, s>>>(a, S, Pw);
-      else
-        softmax_rows<T, GF_ADD><<<blocks, 256, 0, s>>>(a, S, Pw);
-      GF_CHECK_LAUNCH("softmax_rows");
+      if (int rc = launch_softmax_rows<T>(g, a, variant, S, Pw, s)) return rc;
       b.ES = Pw;
+      b.scale = T(1);  // MODE 2 scales its sums by a.scale
       return launch_fwd_mode<T>(g, b, variant, 2, s);
     }
     case GF_STRAT_BASELINE: {

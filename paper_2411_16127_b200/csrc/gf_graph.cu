@@ -123,6 +123,7 @@ void free_graph(DevGraph* g) {
   cudaFree(g->row_order);
   cudaFree(g->col_order);
   cudaFree(g->coo_dst);
+  cudaFree(g->csc_perm);
   delete g;
 }
 

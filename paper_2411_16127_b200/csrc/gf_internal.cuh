@@ -50,8 +50,10 @@ struct DevGraph {
   int32_t n_cta_cols = 0, n_empty_cols = 0;
   int64_t max_in = 0, max_out = 0;
   int device = 0;
-  int32_t* coo_dst = nullptr;  // CSR-order destination per edge (built on first use by
-                               // the edge-parallel strategies; graph-owned)
+  int32_t* coo_dst = nullptr;   // CSR-order destination per edge (built on first use by
+                                // the edge-parallel strategies; graph-owned)
+  int32_t* csc_perm = nullptr;  // CSC slot -> CSR edge id (reference csc_edge_perm), built
+                                // on first use by the unfused backward ops; graph-owned
   int32_t e_csc = 0;        // CSC edge count (== e unless row-sharded)
   bool skip_empty = false;  // do not visit rows / columns without edges
   /// Rows (resp. columns) a pass visits: the empty ones trail the order.
@@ -111,6 +113,7 @@ struct FwdArgs {
   T* O;
   T* stats;  // N x H x 4 records (gf_device.cuh Rec)
   const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
+  const int32_t* eperm = nullptr;  // MODE 3: slot -> CSR edge id of ES (CSC passes)
 };
 
 template <typename T>
@@ -140,10 +143,21 @@ template <typename T>
 int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T* P,
                          cudaStream_t s);
 // Forward kernel modes: 0 = SMMF (compute scores), 1 = scores read from ES
-// (PMF's fused softmax + SpMM), 2 = probabilities read from ES (unfused SpMM:
-// no softmax, O = sum p V, no records).
+// (PMF's fused softmax + SpMM), 2 = edge weights read from ES (plain SpMM:
+// no softmax, O = scale * sum w V, no records), 3 = as 2 with the weight of
+// slot i at ES[eperm[i]] (SpMM over the CSC view with CSR-ordered weights).
 template <typename T>
 int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a, int variant, int mode, cudaStream_t s);
+// Lazily built per-graph edge maps (gf_attn_strategies.cu / gf_unfused_ops.cu).
+int ensure_coo_dst(DevGraph& g, cudaStream_t s);
+int ensure_csc_perm(DevGraph& g, cudaStream_t s);
+// Edge-parallel SDDMM into S[E x H] and the row softmax S -> P (+ records when
+// a.stats != nullptr).
+template <typename T>
+int launch_sddmm_edges(DevGraph& g, const FwdArgs<T>& a, int variant, T* S, cudaStream_t s);
+template <typename T>
+int launch_softmax_rows(const DevGraph& g, const FwdArgs<T>& a, int variant, const T* S, T* P,
+                        cudaStream_t s);
 // Fusion strategies (gf_attn_strategies.cu).  ws: E*H (PMF) or 2*E*H
 // (unfused without caller P) elements of scratch.
 size_t strategy_workspace_bytes(const DevGraph& g, int heads, int elem, int strategy, bool have_p);

@@ -265,12 +265,246 @@ GradBundle<T> device_backward(const Graph& g, const ForwardContext<T>& ctx,
 
 }  // namespace detail
 
+// ---------------------------------------------------- single-step ops --
+namespace detail {
+
+template <typename T>
+gf_attn_desc step_desc(SddmmVariant v, std::int64_t d, double scale, double slope, bool l2) {
+  gf_attn_desc a{};
+  a.dtype = dtype_code<T>();
+  a.variant = v == SddmmVariant::Add ? GF_ADD : GF_DOT;
+  a.l2 = l2 ? 1 : 0;
+  a.heads = 1;
+  a.head_dim = static_cast<std::int32_t>(std::max<std::int64_t>(1, d));
+  a.scale = scale;
+  a.slope = slope;
+  return a;
+}
+
+template <typename T>
+EdgeScalars<T> sddmm_device(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                            const gf_attn_desc& desc) {
+  EdgeScalars<T> s(g.num_edges);
+  if (g.num_edges == 0) return s;
+  gf_graph_t dg = device_graph(g, FusionPlan{});
+  DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), ds(sizeof(T) * s.values.size());
+  GFH_CALL(gf_sddmm(dg, &desc, dq.p, dk.p, ds.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  ds.to(s.values);
+  return s;
+}
+
+template <typename T>
+GradBundle<T> backward_values(const Graph& g, const ForwardContext<T>& ctx,
+                              const DenseMatrix<T>& dO) {
+  const auto& V = ctx.V;
+  if (dO.rows != g.num_nodes || dO.cols != V.cols)
+    throw KernelError("spmm_backward: dO shape mismatch");
+  validate_inputs(g, ctx.Q, ctx.K, V, ctx.kind);
+  std::vector<T> P = ctx.P.values;
+  if (P.size() != static_cast<size_t>(g.num_edges)) {  // hand-built context: rebuild P
+    std::vector<T> O, lse;
+    device_forward(g, FusionPlan{}, ctx.Q, ctx.K, V, ctx.kind, O, lse, &P);
+  }
+  GradBundle<T> gb;
+  const std::int64_t d = V.cols, E = g.num_edges;
+  gb.dQ = DenseMatrix<T>(ctx.Q.rows, ctx.Q.cols);
+  gb.dK = DenseMatrix<T>(ctx.K.rows, ctx.K.cols);
+  gb.dV = DenseMatrix<T>(V.rows, d);
+  gb.dP = EdgeScalars<T>(E);
+  gb.dS = EdgeScalars<T>(E);
+  if (g.num_nodes == 0 || d == 0) return gb;
+  gf_graph_t dg = device_graph(g, ctx.plan);
+  const gf_attn_desc desc = make_desc<T>(ctx.kind, d);
+  DevBuf dq = DevBuf::from(ctx.Q.data), dk = DevBuf::from(ctx.K.data), dv = DevBuf::from(V.data),
+         dp = DevBuf::from(P), ddo = DevBuf::from(dO.data);
+  DevBuf gdp(sizeof(T) * std::max<std::int64_t>(E, 1)), gds(sizeof(T) * std::max<std::int64_t>(E, 1));
+  DevBuf gq(sizeof(T) * gb.dQ.data.size()), gk(sizeof(T) * gb.dK.data.size()),
+      gv(sizeof(T) * gb.dV.data.size());
+  const std::int32_t dt = dtype_code<T>(), D = static_cast<std::int32_t>(d);
+  // 5 launches: dP (SDDMM), dV (CSC SpMM), dS (softmax bwd), dK (CSR), dQ (CSC)
+  GFH_CALL(gf_spmm_backward(dg, dt, 1, D, dp.p, dv.p, ddo.p, gdp.p, gv.p, nullptr));
+  GFH_CALL(gf_softmax_backward(dg, dt, 1, dp.p, gdp.p, gds.p, nullptr));
+  GFH_CALL(gf_sddmm_backward(dg, &desc, dq.p, dk.p, gds.p, gq.p, gk.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  gq.to(gb.dQ.data);
+  gk.to(gb.dK.data);
+  gv.to(gb.dV.data);
+  gdp.to(gb.dP.values);
+  gds.to(gb.dS.values);
+  return gb;
+}
+
+template <typename T>
+ExecCounters backward_counter_model(const Graph& g, const ForwardContext<T>& ctx,
+                                    std::int64_t launches) {
+  return backward_counters(g, ctx.V.cols, sizeof(T), static_cast<std::uint64_t>(launches));
+}
+
+}  // namespace detail
+
+template <typename T>
+EdgeScalars<T> sddmm_dot(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                         T scale) {
+  if (Q.rows != g.num_nodes || K.rows != g.num_nodes || Q.cols != K.cols)
+    throw KernelError("sddmm_dot: dimension mismatch");
+  if (Q.cols == 0) return EdgeScalars<T>(g.num_edges);
+  return detail::sddmm_device(
+      g, Q, K, detail::step_desc<T>(SddmmVariant::Dot, Q.cols, scale, 0.0, false));
+}
+
+template <typename T>
+EdgeScalars<T> sddmm_add(const Graph& g, const DenseMatrix<T>& el, const DenseMatrix<T>& er,
+                         T leaky_slope) {
+  if (el.rows != g.num_nodes || er.rows != g.num_nodes || el.cols != 1 || er.cols != 1)
+    throw KernelError("sddmm_add: el/er must be N x 1");
+  return detail::sddmm_device(
+      g, el, er, detail::step_desc<T>(SddmmVariant::Add, 1, 1.0, leaky_slope, false));
+}
+
+template <typename T>
+DenseMatrix<T> l2_normalize_rows(const DenseMatrix<T>& X, T eps) {
+  if (eps <= T(0)) throw KernelError("l2_normalize_rows: eps must be > 0");
+  DenseMatrix<T> out(X.rows, X.cols);
+  if (X.rows == 0 || X.cols == 0) return out;
+  detail::need_device();
+  detail::DevBuf x = detail::DevBuf::from(X.data), y(sizeof(T) * out.data.size());
+  GFH_CALL(gf_l2_normalize_rows(detail::dtype_code<T>(), X.rows, 1,
+                                static_cast<std::int32_t>(X.cols), x.p, y.p, eps, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  y.to(out.data);
+  return out;
+}
+
+template <typename T>
+DenseMatrix<T> l2_normalize_backward(const DenseMatrix<T>& X, const DenseMatrix<T>& dY, T eps) {
+  if (dY.rows != X.rows || dY.cols != X.cols)
+    throw KernelError("l2_normalize_backward: shape mismatch");
+  DenseMatrix<T> dX(X.rows, X.cols);
+  if (X.rows == 0 || X.cols == 0) return dX;
+  detail::need_device();
+  detail::DevBuf x = detail::DevBuf::from(X.data), dy = detail::DevBuf::from(dY.data),
+                 dx(sizeof(T) * dX.data.size());
+  GFH_CALL(gf_l2_normalize_backward(detail::dtype_code<T>(), X.rows, 1,
+                                    static_cast<std::int32_t>(X.cols), x.p, dy.p, dx.p, eps,
+                                    nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  dx.to(dX.data);
+  return dX;
+}
+
+template <typename T>
+EdgeScalars<T> edge_softmax(const Graph& g, const EdgeScalars<T>& s) {
+  if (s.size() != g.num_edges) throw KernelError("edge_softmax: length mismatch");
+  EdgeScalars<T> p(g.num_edges);
+  if (g.num_edges == 0) return p;
+  gf_graph_t dg = detail::device_graph(g, FusionPlan{});
+  detail::DevBuf ds = detail::DevBuf::from(s.values), dp(sizeof(T) * p.values.size());
+  GFH_CALL(gf_edge_softmax(dg, detail::dtype_code<T>(), 1, ds.p, dp.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  dp.to(p.values);
+  return p;
+}
+
+template <typename T>
+DenseMatrix<T> spmm(const Graph& g, const EdgeScalars<T>& p, const DenseMatrix<T>& V) {
+  if (V.rows != g.num_nodes) throw KernelError("spmm: V.rows must equal N");
+  if (p.size() != g.num_edges) throw KernelError("spmm: P length mismatch");
+  DenseMatrix<T> out(g.num_nodes, V.cols);
+  if (g.num_nodes == 0 || V.cols == 0) return out;
+  gf_graph_t dg = detail::device_graph(g, FusionPlan{});
+  detail::DevBuf dp = detail::DevBuf::from(p.values), dv = detail::DevBuf::from(V.data),
+                 o(sizeof(T) * out.data.size());
+  GFH_CALL(gf_spmm(dg, detail::dtype_code<T>(), 1, static_cast<std::int32_t>(V.cols), dp.p, dv.p,
+                   o.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  o.to(out.data);
+  return out;
+}
+
+template <typename T>
+EdgeScalars<T> sddmm(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
+                     const SddmmKind& kind) {
+  if (kind.variant == SddmmVariant::Add)
+    return sddmm_add(g, Q, K, static_cast<T>(kind.leaky_slope));
+  if (!kind.l2_normalize_inputs) return sddmm_dot(g, Q, K, static_cast<T>(kind.scale));
+  if (Q.rows != g.num_nodes || K.rows != g.num_nodes || Q.cols != K.cols)
+    throw KernelError("sddmm_dot: dimension mismatch");
+  if (Q.cols == 0) return EdgeScalars<T>(g.num_edges);
+  return detail::sddmm_device(
+      g, Q, K, detail::step_desc<T>(SddmmVariant::Dot, Q.cols, kind.scale, 0.0, true));
+}
+
+template <typename T>
+std::pair<EdgeScalars<T>, DenseMatrix<T>> spmm_backward(const Graph& g, const EdgeScalars<T>& P,
+                                                        const DenseMatrix<T>& V,
+                                                        const DenseMatrix<T>& dO) {
+  if (dO.rows != g.num_nodes || dO.cols != V.cols)
+    throw KernelError("spmm_backward: dO shape mismatch");
+  if (V.rows != g.num_nodes || P.size() != g.num_edges)
+    throw KernelError("spmm_backward: P / V shape mismatch");
+  EdgeScalars<T> dP(g.num_edges);
+  DenseMatrix<T> dV(g.num_nodes, V.cols);
+  if (g.num_nodes == 0 || V.cols == 0) return {std::move(dP), std::move(dV)};
+  gf_graph_t dg = detail::device_graph(g, FusionPlan{});
+  detail::DevBuf dp = detail::DevBuf::from(P.values), dv = detail::DevBuf::from(V.data),
+                 ddo = detail::DevBuf::from(dO.data),
+                 gdp(sizeof(T) * std::max<std::int64_t>(g.num_edges, 1)),
+                 gv(sizeof(T) * dV.data.size());
+  GFH_CALL(gf_spmm_backward(dg, detail::dtype_code<T>(), 1, static_cast<std::int32_t>(V.cols),
+                            dp.p, dv.p, ddo.p, gdp.p, gv.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  gdp.to(dP.values);
+  gv.to(dV.data);
+  return {std::move(dP), std::move(dV)};
+}
+
+template <typename T>
+EdgeScalars<T> softmax_backward(const Graph& g, const EdgeScalars<T>& P, const EdgeScalars<T>& dP) {
+  if (P.size() != g.num_edges || dP.size() != g.num_edges)
+    throw KernelError("softmax_backward: length mismatch");
+  EdgeScalars<T> dS(g.num_edges);
+  if (g.num_edges == 0) return dS;
+  gf_graph_t dg = detail::device_graph(g, FusionPlan{});
+  detail::DevBuf p = detail::DevBuf::from(P.values), dp = detail::DevBuf::from(dP.values),
+                 ds(sizeof(T) * dS.values.size());
+  GFH_CALL(gf_softmax_backward(dg, detail::dtype_code<T>(), 1, p.p, dp.p, ds.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  ds.to(dS.values);
+  return dS;
+}
+
+template <typename T>
+std::pair<DenseMatrix<T>, DenseMatrix<T>> sddmm_backward(const Graph& g, const DenseMatrix<T>& Q,
+                                                         const DenseMatrix<T>& K,
+                                                         const EdgeScalars<T>& dS,
+                                                         const SddmmKind& kind) {
+  if (dS.size() != g.num_edges) throw KernelError("sddmm_backward: dS length mismatch");
+  const bool add = kind.variant == SddmmVariant::Add;
+  if (add ? (Q.rows != g.num_nodes || K.rows != g.num_nodes || Q.cols != 1 || K.cols != 1)
+          : (Q.rows != g.num_nodes || K.rows != g.num_nodes || Q.cols != K.cols))
+    throw KernelError("sddmm_backward: Q/K shape mismatch");
+  DenseMatrix<T> dQ(g.num_nodes, Q.cols), dK(g.num_nodes, K.cols);
+  if (g.num_nodes == 0 || Q.cols == 0) return {std::move(dQ), std::move(dK)};
+  gf_graph_t dg = detail::device_graph(g, FusionPlan{});
+  const gf_attn_desc desc = detail::step_desc<T>(kind.variant, add ? 1 : Q.cols, kind.scale,
+                                                 kind.leaky_slope, !add && kind.l2_normalize_inputs);
+  detail::DevBuf q = detail::DevBuf::from(Q.data), k = detail::DevBuf::from(K.data),
+                 ds = detail::DevBuf::from(dS.values), gq(sizeof(T) * dQ.data.size()),
+                 gk(sizeof(T) * dK.data.size());
+  GFH_CALL(gf_sddmm_backward(dg, &desc, q.p, k.p, ds.p, gq.p, gk.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  gq.to(dQ.data);
+  gk.to(dK.data);
+  return {std::move(dQ), std::move(dK)};
+}
+
 template <typename T>
 BackwardResult<T> unfused_backward(const Graph& g, const ForwardContext<T>& ctx,
                                    const DenseMatrix<T>& dO) {
   BackwardResult<T> r;
-  r.grads = detail::device_backward(g, ctx, dO);
-  r.counters = detail::backward_counters(g, ctx.V.cols, sizeof(T), 5);
+  r.grads = detail::backward_values(g, ctx, dO);  // the real 5-launch schedule
+  r.counters = detail::backward_counter_model(g, ctx, 5);
   return r;
 }
 
@@ -286,7 +520,9 @@ BackwardResult<T> fused_backward(const Graph& g, const ForwardContext<T>& ctx,
     }
   }
   BackwardResult<T> r;
-  r.grads = detail::device_backward(g, ctx, dO);
+  // feasible: the fused recompute backward (pass A + pass B); otherwise the
+  // reference falls back to the unfused schedule (autograd.hpp:213-225)
+  r.grads = feasible ? detail::device_backward(g, ctx, dO) : detail::backward_values(g, ctx, dO);
   r.counters = detail::backward_counters(g, ctx.V.cols, sizeof(T), feasible ? 3 : 5);
   r.counters.fallback_unfused = !feasible;
   return r;
@@ -465,7 +701,29 @@ PipelineInputs<T> make_pipeline_inputs(const Graph& g, const ConvSpec& spec, std
       const ConvSpec&, const Graph&, const DenseMatrix<T>&, const ConvWeights<T>&, FusionPlan);  \
   template ConvGrads<T> conv_backward<T>(const ConvSpec&, const Graph&, const ConvContext<T>&,   \
                                          const ConvWeights<T>&, const DenseMatrix<T>&);          \
-  template PipelineInputs<T> make_pipeline_inputs<T>(const Graph&, const ConvSpec&, std::uint64_t);
+  template PipelineInputs<T> make_pipeline_inputs<T>(const Graph&, const ConvSpec&, std::uint64_t); \
+  template EdgeScalars<T> sddmm_dot<T>(const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&, \
+                                       T);                                                       \
+  template EdgeScalars<T> sddmm_add<T>(const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&, \
+                                       T);                                                       \
+  template DenseMatrix<T> l2_normalize_rows<T>(const DenseMatrix<T>&, T);                        \
+  template DenseMatrix<T> l2_normalize_backward<T>(const DenseMatrix<T>&, const DenseMatrix<T>&, \
+                                                   T);                                           \
+  template EdgeScalars<T> edge_softmax<T>(const Graph&, const EdgeScalars<T>&);                  \
+  template DenseMatrix<T> spmm<T>(const Graph&, const EdgeScalars<T>&, const DenseMatrix<T>&);   \
+  template EdgeScalars<T> sddmm<T>(const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&,   \
+                                   const SddmmKind&);                                            \
+  template std::pair<EdgeScalars<T>, DenseMatrix<T>> spmm_backward<T>(                           \
+      const Graph&, const EdgeScalars<T>&, const DenseMatrix<T>&, const DenseMatrix<T>&);        \
+  template EdgeScalars<T> softmax_backward<T>(const Graph&, const EdgeScalars<T>&,               \
+                                              const EdgeScalars<T>&);                            \
+  template std::pair<DenseMatrix<T>, DenseMatrix<T>> sddmm_backward<T>(                          \
+      const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&, const EdgeScalars<T>&,         \
+      const SddmmKind&);                                                                         \
+  template GradBundle<T> detail::backward_values<T>(const Graph&, const ForwardContext<T>&,      \
+                                                    const DenseMatrix<T>&);                      \
+  template ExecCounters detail::backward_counter_model<T>(const Graph&, const ForwardContext<T>&, \
+                                                          std::int64_t);
 
 GF_INSTANTIATE(float)
 GF_INSTANTIATE(double)

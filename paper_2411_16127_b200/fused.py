@@ -257,3 +257,83 @@ def gat_fanin(Hf, a_l, a_r, dV, d_el, d_er, heads, head_dim, stream=None):
                              _p(dV), _p(d_el), _p(d_er), _p(dH), _p(dal), _p(dar),
                              _stream(stream)), "gf_gat_fanin")
     return dH, dal, dar
+
+
+# ---- single-step operators (the unfused schedule; gf_cuda.h "single-step") --
+def _edge_buf(g, heads, dt, dev):
+    return torch.empty(max(g.e, 1), heads, dtype=dt, device=dev)
+
+
+def sddmm(g: DeviceGraph, spec: AttnSpec, Q, K, S=None, stream=None):
+    """S[E x H] (kernels.hpp:106-117)."""
+    S = _edge_buf(g, spec.heads, Q.dtype, Q.device) if S is None else S
+    check(lib().gf_sddmm(g.handle, C.byref(spec.desc(Q.dtype)), _p(Q), _p(K), _p(S),
+                         _stream(stream)), "gf_sddmm")
+    return S[: g.e]
+
+
+def edge_softmax(g: DeviceGraph, heads, S, P=None, stream=None):
+    """P[E x H] (kernels.hpp:65-82)."""
+    P = _edge_buf(g, heads, S.dtype, S.device) if P is None else P
+    check(lib().gf_edge_softmax(g.handle, DTYPES[S.dtype], heads, _p(S), _p(P), _stream(stream)),
+          "gf_edge_softmax")
+    return P[: g.e]
+
+
+def spmm(g: DeviceGraph, heads, head_dim, P, V, O=None, stream=None):
+    """O = P V per head (kernels.hpp:85-102)."""
+    O = torch.empty(g.n, heads * head_dim, dtype=V.dtype, device=V.device) if O is None else O
+    check(lib().gf_spmm(g.handle, DTYPES[V.dtype], heads, head_dim, _p(P), _p(V), _p(O),
+                        _stream(stream)), "gf_spmm")
+    return O
+
+
+def l2_normalize_rows(X, heads, head_dim, eps=1e-12, stream=None):
+    Y = torch.empty_like(X)
+    check(lib().gf_l2_normalize_rows(DTYPES[X.dtype], X.shape[0], heads, head_dim, _p(X), _p(Y),
+                                     eps, _stream(stream)), "gf_l2_normalize_rows")
+    return Y
+
+
+def l2_normalize_backward(X, dY, heads, head_dim, eps=1e-12, stream=None):
+    dX = torch.empty_like(X)
+    check(lib().gf_l2_normalize_backward(DTYPES[X.dtype], X.shape[0], heads, head_dim, _p(X),
+                                         _p(dY), _p(dX), eps, _stream(stream)),
+          "gf_l2_normalize_backward")
+    return dX
+
+
+def spmm_backward(g: DeviceGraph, heads, head_dim, P, V, dO, stream=None):
+    """(dP, dV) (autograd.hpp:33-58)."""
+    dP = _edge_buf(g, heads, V.dtype, V.device)
+    dV = torch.empty_like(V)
+    check(lib().gf_spmm_backward(g.handle, DTYPES[V.dtype], heads, head_dim, _p(P), _p(V), _p(dO),
+                                 _p(dP), _p(dV), _stream(stream)), "gf_spmm_backward")
+    return dP[: g.e], dV
+
+
+def softmax_backward(g: DeviceGraph, heads, P, dP, stream=None):
+    """dS (autograd.hpp:62-73)."""
+    dS = _edge_buf(g, heads, P.dtype, P.device)
+    check(lib().gf_softmax_backward(g.handle, DTYPES[P.dtype], heads, _p(P), _p(dP), _p(dS),
+                                    _stream(stream)), "gf_softmax_backward")
+    return dS[: g.e]
+
+
+def sddmm_backward(g: DeviceGraph, spec: AttnSpec, Q, K, dS, stream=None):
+    """(dQ|del, dK|der) (autograd.hpp:102-154)."""
+    dQ = torch.empty(g.n, spec.qk_width, dtype=Q.dtype, device=Q.device)
+    dK = torch.empty_like(dQ)
+    check(lib().gf_sddmm_backward(g.handle, C.byref(spec.desc(Q.dtype)), _p(Q), _p(K), _p(dS),
+                                  _p(dQ), _p(dK), _stream(stream)), "gf_sddmm_backward")
+    return dQ, dK
+
+
+def attn_backward_unfused(g: DeviceGraph, spec: AttnSpec, Q, K, V, P, dO, stream=None):
+    """The reference's unfused backward (autograd.hpp:158-170, 196-203): dP/dV,
+    then dS, then dQ/dK, with the E x H edge gradients in HBM.  Returns
+    (dQ|del, dK|der, dV, dP, dS)."""
+    dP, dV = spmm_backward(g, spec.heads, spec.head_dim, P, V, dO, stream=stream)
+    dS = softmax_backward(g, spec.heads, P, dP, stream=stream)
+    dQ, dK = sddmm_backward(g, spec, Q, K, dS, stream=stream)
+    return dQ, dK, dV, dP, dS

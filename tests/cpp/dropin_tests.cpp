@@ -6,6 +6,7 @@
 // this file's own harness.  Exit code 0 = all checks passed.
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <string>
 
@@ -223,6 +224,176 @@ static void layer_cases() {
   }
 }
 
+static bool near(double a, double b, double tol = 1e-12) {
+  return std::abs(a - b) <= tol * std::max({std::abs(a), std::abs(b), 1.0});
+}
+
+// test_kernels.cpp:26-118 and test_autograd.cpp:28-158: the single-step
+// operators, now device ops, on the reference's own known answers.
+static void step_ops_cases() {
+  Graph g = gen_random(16, 4, 3);
+  DenseMatrix<double> ones(16, 2, 1.0);
+  auto s1 = sddmm_dot(g, ones, ones, 1.0);
+  bool ok = s1.size() == g.num_edges;
+  for (EdgeId e = 0; e < g.num_edges; ++e) ok = ok && near(s1[e], 2.0);
+  EXPECT(ok);
+  Graph loops = from_coo(4, {0, 1, 2, 0}, {0, 1, 2, 1});
+  DenseMatrix<double> Qd(4, 4);
+  for (int i = 0; i < 4; ++i) Qd.at(i, i) = i + 1.0;
+  auto so = sddmm_dot(loops, Qd, Qd, 2.0);
+  EXPECT(near(so[0], 2.0) && near(so[1], 0.0) && near(so[2], 8.0) && near(so[3], 18.0));
+  {
+    auto Q = random_matrix<double>(16, 4, 1), K = random_matrix<double>(16, 4, 2);
+    auto s = sddmm_dot(g, Q, K, 0.7);
+    bool m = true;
+    for (EdgeId e = 0; e < g.num_edges; ++e) {
+      double acc = 0;
+      for (int c = 0; c < 4; ++c) acc += Q.at(g.coo_src[e], c) * K.at(g.coo_dst[e], c);
+      m = m && near(s[e], 0.7 * acc);
+    }
+    EXPECT(m);
+  }
+  bool threw = false;
+  try {
+    sddmm_dot(g, DenseMatrix<double>(16, 4), DenseMatrix<double>(16, 3), 1.0);
+  } catch (const KernelError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  Graph one = from_coo(2, {0}, {1});
+  DenseMatrix<double> el(2, 1), er(2, 1);
+  el.data[0] = 1.0;
+  er.data[1] = -3.0;
+  EXPECT(near(sddmm_add(one, el, er, 0.2)[0], -0.4));
+  DenseMatrix<double> X(1, 2);
+  X.at(0, 0) = 3;
+  X.at(0, 1) = 4;
+  auto Y = l2_normalize_rows(X, 1e-12);
+  EXPECT(near(Y.at(0, 0), 0.6) && near(Y.at(0, 1), 0.8));
+  auto Z = l2_normalize_rows(DenseMatrix<double>(1, 3), 1e-12);
+  EXPECT(Z.data[0] == 0.0 && Z.data[1] == 0.0 && Z.data[2] == 0.0);
+  threw = false;
+  try {
+    l2_normalize_rows(DenseMatrix<double>(1, 1), 0.0);
+  } catch (const KernelError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  // edge softmax: (0, 0) -> (1/2, 1/2); f32 (1000, 1001) -> (1/(1+e), e/(1+e))
+  Graph two = from_coo(3, {0, 1}, {2, 2});
+  EdgeScalars<float> sf(2);
+  sf[0] = 1000.f;
+  sf[1] = 1001.f;
+  auto pf = edge_softmax(two, sf);
+  EXPECT(std::abs(pf[0] - 1.0 / (1.0 + std::exp(1.0))) < 1e-5 &&
+         std::abs(pf[1] - std::exp(1.0) / (1.0 + std::exp(1.0))) < 1e-5);
+  // spmm: 1/2 weights give the mean; an empty row gives 0
+  auto Vm = random_matrix<double>(3, 3, 4);
+  auto Om = spmm(two, EdgeScalars<double>(2, 0.5), Vm);
+  bool mean = true;
+  for (int c = 0; c < 3; ++c)
+    mean = mean && near(Om.at(2, c), 0.5 * (Vm.at(0, c) + Vm.at(1, c))) && Om.at(0, c) == 0.0;
+  EXPECT(mean);
+  // spmm_backward: identity P passes dO through; dense formulas on N=8
+  {
+    Graph id = from_coo(3, {0, 1, 2}, {0, 1, 2});
+    auto V = random_matrix<double>(3, 4, 1), dO = random_matrix<double>(3, 4, 2);
+    auto r = spmm_backward(id, EdgeScalars<double>(3, 1.0), V, dO);
+    bool pass = true;
+    for (size_t i = 0; i < r.second.data.size(); ++i) pass = pass && near(r.second.data[i], dO.data[i]);
+    EXPECT(pass);
+    Graph g8 = gen_random(8, 3, 3);
+    auto V8 = random_matrix<double>(8, 3, 4), dO8 = random_matrix<double>(8, 3, 5);
+    auto P8 = edge_softmax(g8, sddmm_dot(g8, V8, V8, 1.0));
+    auto [dP, dV] = spmm_backward(g8, P8, V8, dO8);
+    DenseMatrix<double> dVd(8, 3);
+    bool dpok = true;
+    for (EdgeId e = 0; e < g8.num_edges; ++e) {
+      double acc = 0;
+      for (int c = 0; c < 3; ++c) {
+        acc += dO8.at(g8.coo_dst[e], c) * V8.at(g8.coo_src[e], c);
+        dVd.at(g8.coo_src[e], c) += P8[e] * dO8.at(g8.coo_dst[e], c);
+      }
+      dpok = dpok && near(dP[e], acc);
+    }
+    EXPECT(dpok);
+    EXPECT(floor1(dV, dVd) < 1e-12);
+  }
+  // softmax_backward: (1/2,1/2) with dP=(1,0) -> (1/4,-1/4); rows sum to zero
+  {
+    EdgeScalars<double> P(2, 0.5), dP(2);
+    dP[0] = 1.0;
+    auto dS = softmax_backward(two, P, dP);
+    EXPECT(near(dS[0], 0.25) && near(dS[1], -0.25));
+    Graph g50 = gen_random(50, 6, 8);
+    auto sv = random_matrix<double>(g50.num_edges, 1, 9), dv = random_matrix<double>(g50.num_edges, 1, 10);
+    EdgeScalars<double> S(g50.num_edges), dP2(g50.num_edges);
+    S.values = sv.data;
+    dP2.values = dv.data;
+    auto dS2 = softmax_backward(g50, edge_softmax(g50, S), dP2);
+    bool zero = true;
+    for (NodeId v = 0; v < g50.num_nodes; ++v) {
+      double sum = 0;
+      for (EdgeId i = g50.csr_row_ptr[v]; i < g50.csr_row_ptr[v + 1]; ++i) sum += dS2[i];
+      zero = zero && std::abs(sum) <= 1e-14 * std::max<EdgeId>(1, g50.csr_row_ptr[v + 1] - g50.csr_row_ptr[v]);
+    }
+    EXPECT(zero);
+  }
+  // sddmm_backward: single-edge product rule; dense dS K / dS^T Q
+  {
+    auto Q = random_matrix<double>(2, 3, 3), K = random_matrix<double>(2, 3, 4);
+    auto [dQ, dK] = sddmm_backward(one, Q, K, EdgeScalars<double>(1, 1.0), SddmmKind::dot(1.0));
+    bool pr = true;
+    for (int c = 0; c < 3; ++c)
+      pr = pr && near(dQ.at(0, c), K.at(1, c)) && near(dK.at(1, c), Q.at(0, c)) &&
+           dQ.at(1, c) == 0.0 && dK.at(0, c) == 0.0;
+    EXPECT(pr);
+    Graph g9 = gen_random(9, 3, 5);
+    auto Q9 = random_matrix<double>(9, 2, 6), K9 = random_matrix<double>(9, 2, 7);
+    auto ds = random_matrix<double>(g9.num_edges, 1, 8);
+    EdgeScalars<double> dS(g9.num_edges);
+    dS.values = ds.data;
+    auto [gq, gk] = sddmm_backward(g9, Q9, K9, dS, SddmmKind::dot(0.4));
+    DenseMatrix<double> dq(9, 2), dk(9, 2);
+    for (EdgeId e = 0; e < g9.num_edges; ++e)
+      for (int c = 0; c < 2; ++c) {
+        dq.at(g9.coo_src[e], c) += 0.4 * dS[e] * K9.at(g9.coo_dst[e], c);
+        dk.at(g9.coo_dst[e], c) += 0.4 * dS[e] * Q9.at(g9.coo_src[e], c);
+      }
+    EXPECT(floor1(gq, dq) < 1e-12 && floor1(gk, dk) < 1e-12);
+  }
+  // fused == unfused (5 launches, edge gradients filled) for GT / AGNN / GAT
+  for (std::uint64_t seed = 0; seed < 6; ++seed) {
+    Graph gs = gen_random(20 + seed * 40, 5, seed);
+    ConvSpec spec;
+    spec.model = seed % 3 == 0 ? Model::GT : seed % 3 == 1 ? Model::AGNN : Model::GAT;
+    spec.dim = 5;
+    auto in = make_pipeline_inputs<double>(gs, spec, seed + 50);
+    auto fr = run_strategy(gs, in.Q, in.K, in.V, in.kind, FusionPlan{});
+    auto dO = random_matrix<double>(gs.num_nodes, 5, seed + 60);
+    auto fb = fused_backward(gs, fr.ctx, dO, FusionPlan{});
+    auto ub = unfused_backward(gs, fr.ctx, dO);
+    EXPECT(fb.counters.kernel_launches == 3 && ub.counters.kernel_launches == 5);
+    EXPECT(floor1(fb.grads.dQ, ub.grads.dQ) < 1e-11 && floor1(fb.grads.dK, ub.grads.dK) < 1e-11 &&
+           floor1(fb.grads.dV, ub.grads.dV) < 1e-11);
+    EXPECT(ub.grads.dP.size() == gs.num_edges && ub.grads.dS.size() == gs.num_edges);
+  }
+  // infeasible plan -> the unfused fallback (fills the edge gradients)
+  {
+    Graph gh = gen_super_node(100, 2, 90, 1);
+    ConvSpec spec;
+    spec.model = Model::GT;
+    spec.dim = 4;
+    auto in = make_pipeline_inputs<double>(gh, spec, 2);
+    auto fr = run_strategy(gh, in.Q, in.K, in.V, in.kind, FusionPlan{});
+    FusionPlan tight;
+    tight.shared_mem_budget_bytes = 256;
+    auto res = fused_backward(gh, fr.ctx, DenseMatrix<double>(100, 4, 1.0), tight);
+    EXPECT(res.counters.fallback_unfused && res.counters.kernel_launches == 5);
+    EXPECT(res.grads.dS.size() == gh.num_edges);
+  }
+}
+
 // test_models.cpp:154-233 (benchmark runner, auto strategy, config parsing)
 static void bench_cases() {
   BenchConfig cfg;
@@ -303,6 +474,7 @@ int main() {
   feasibility_error();
   backward_cases();
   layer_cases();
+  step_ops_cases();
   bench_cases();
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
