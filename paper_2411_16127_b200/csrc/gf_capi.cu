@@ -8,6 +8,20 @@ namespace {
 thread_local std::string t_err;
 }
 void set_error(const std::string& msg) { t_err = msg; }
+
+cudaError_t scratch_alloc_raw(void** p, size_t bytes, cudaStream_t s) {
+  static bool tuned[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !tuned[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = uint64_t(8) << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    tuned[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
 }  // namespace gfb
 
 
@@ -185,7 +199,7 @@ extern "C" int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int3
   void* ws = workspace;
   bool own = false;
   if (need > 0 && !ws) {
-    GF_CHECK_CUDA(cudaMallocAsync(&ws, need, s));
+    GF_CHECK_CUDA(gfb::scratch_alloc(&ws, need, s));
     own = true;
   } else if (need > workspace_bytes) {
     gfb::set_error("gf_attn_fwd_strategy: workspace too small (see gf_attn_fwd_workspace)");
@@ -215,7 +229,7 @@ extern "C" int gf_time_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int3
   size_t need = 0;
   if (int rc = gf_attn_fwd_workspace(g, desc, strategy, 0, &need)) return rc;
   void* ws = nullptr;
-  if (need) GF_CHECK_CUDA(cudaMallocAsync(&ws, need, s));
+  if (need) GF_CHECK_CUDA(gfb::scratch_alloc(&ws, need, s));
   cudaEvent_t a = nullptr, b = nullptr;
   int rc = GF_OK;
   if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {

@@ -123,7 +123,7 @@ int gemm_impl(int trans, int64_t M, int64_t N, int64_t K, const T* A, const T* B
   splits = static_cast<int>((K + kper - 1) / kper);
   if (splits < 1) splits = 1;
   T* part = nullptr;
-  if (splits > 1) GF_CHECK_CUDA(cudaMallocAsync(&part, sizeof(T) * splits * M * N, s));
+  if (splits > 1) GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(T) * splits * M * N, s));
   dim3 grid(tn, tm, splits);
   if (trans)
     gemm_tile<T, true><<<grid, 256, 0, s>>>(static_cast<int>(M), static_cast<int>(N),
@@ -273,7 +273,7 @@ int fanin_impl(int64_t n, int H, int D, const T* Hf, const T* al, const T* ar, c
   const int64_t rpb = 512;
   const int blocks = static_cast<int>(std::max<int64_t>(1, (n + rpb - 1) / rpb));
   T* part = nullptr;
-  GF_CHECK_CUDA(cudaMallocAsync(&part, sizeof(T) * blocks * 2 * F, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(T) * blocks * 2 * F, s));
   gfb::gat_da_partial<T><<<blocks, 128, 0, s>>>(n, H, D, rpb, Hf, del, der, part);
   GF_CHECK_LAUNCH("gat_da_partial");
   gfb::gat_da_reduce<T><<<(2 * F + 255) / 256, 256, 0, s>>>(blocks, F, part, dal, dar);

@@ -69,10 +69,10 @@ int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32
     return GF_OK;
   }
   int32_t *deg = nullptr, *ids = nullptr, *deg_sorted = nullptr, *stats = nullptr;
-  GF_CHECK_CUDA(cudaMallocAsync(&deg, sizeof(int32_t) * n, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&ids, sizeof(int32_t) * n, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&deg_sorted, sizeof(int32_t) * n, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&stats, sizeof(int32_t) * 4, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&deg, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&ids, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&deg_sorted, sizeof(int32_t) * n, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&stats, sizeof(int32_t) * 4, s));
   GF_CHECK_CUDA(cudaMemsetAsync(stats, 0, sizeof(int32_t) * 4, s));
   degrees_kernel<<<(n + 255) / 256, 256, 0, s>>>(d_ptr, n, deg, ids);
   GF_CHECK_LAUNCH("degrees_kernel");
@@ -89,7 +89,7 @@ int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32
   GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted,
                                                            ids, d_order, n, 0, end_bit, s));
   void* tmp = nullptr;
-  GF_CHECK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&tmp, tmp_bytes, s));
   GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, ids,
                                                            d_order, n, 0, end_bit, s));
   GF_CHECK_LAUNCH("radix sort");
@@ -330,11 +330,11 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
   uint64_t *k_ds = nullptr, *k_sd = nullptr, *k_ds_s = nullptr, *k_sd_s = nullptr;
   unsigned long long* flags = nullptr;
   const size_t eb = sizeof(uint64_t) * (e > 0 ? e : 1);
-  GF_CHECK_CUDA(cudaMallocAsync(&k_ds, eb, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&k_sd, eb, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&k_ds_s, eb, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&k_sd_s, eb, s));
-  GF_CHECK_CUDA(cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&k_ds, eb, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&k_sd, eb, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&k_ds_s, eb, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&k_sd_s, eb, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&flags, 2 * sizeof(unsigned long long), s));
   GF_CHECK_CUDA(cudaMemsetAsync(flags, 0xff, 2 * sizeof(unsigned long long), s));
   int rc = GF_OK;
   unsigned long long hflags[2] = {~0ull, ~0ull};
@@ -344,7 +344,7 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
     size_t tb = 0;
     GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, k_ds, k_ds_s, e, 0, 2 * b, s));
     void* tmp = nullptr;
-    GF_CHECK_CUDA(cudaMallocAsync(&tmp, tb, s));
+    GF_CHECK_CUDA(gfb::scratch_alloc(&tmp, tb, s));
     size_t t = tb;
     GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t, k_ds, k_ds_s, e, 0, 2 * b, s));
     t = tb;

@@ -386,7 +386,7 @@ int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, 
   ks = ((ks + TC_KC - 1) / TC_KC) * TC_KC;
   const int splits = static_cast<int>((K + ks - 1) / ks);
   float* part = nullptr;
-  GF_CHECK_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * M * N, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(float) * splits * M * N, s));
   const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC +
                                       TC_M * static_cast<size_t>(N + 4));
   GF_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_tn_3xtf32,

@@ -123,40 +123,49 @@ __global__ void __launch_bounds__(256) add_grad(const int32_t* __restrict__ ptr,
 }
 
 // Per-head row L2 normalisation y = x / max(||x||, eps) (kernels.hpp:50-61)
-// and its backward (autograd.hpp:76-95); one thread per (node, head).
+// and its backward (autograd.hpp:76-95); one warp per (node, head) row with
+// lanes over the D features (coalesced), sums by warp shuffles.
 template <typename T>
-__global__ void l2_rows(int64_t n, int H, int D, const T* __restrict__ X, T* __restrict__ Y,
-                        T eps) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * H;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const T* x = X + i * D;
-    T* y = Y + i * D;
+__device__ __forceinline__ T warp_sum(T x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) l2_rows(int64_t rows, int D, const T* __restrict__ X,
+                                               T* __restrict__ Y, T eps) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const T* x = X + r * D;
     T sq = T(0);
-    for (int c = 0; c < D; ++c) sq += x[c] * x[c];
-    const T nrm = sqrt(sq);
+    for (int c = lane; c < D; c += 32) sq += x[c] * x[c];
+    const T nrm = sqrt(warp_sum(sq));
     const T den = nrm < eps ? eps : nrm;
-    for (int c = 0; c < D; ++c) y[c] = x[c] / den;
+    for (int c = lane; c < D; c += 32) Y[r * D + c] = x[c] / den;
   }
 }
 
 template <typename T>
-__global__ void l2_rows_bwd(int64_t n, int H, int D, const T* __restrict__ X,
-                            const T* __restrict__ dY, T* __restrict__ dX, T eps) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * H;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const T* x = X + i * D;
-    const T* dy = dY + i * D;
-    T* dx = dX + i * D;
+__global__ void __launch_bounds__(256) l2_rows_bwd(int64_t rows, int D, const T* __restrict__ X,
+                                                   const T* __restrict__ dY, T* __restrict__ dX,
+                                                   T eps) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const T* x = X + r * D;
+    const T* dy = dY + r * D;
     T sq = T(0);
-    for (int c = 0; c < D; ++c) sq += x[c] * x[c];
-    const T nrm = sqrt(sq);
+    for (int c = lane; c < D; c += 32) sq += x[c] * x[c];
+    const T nrm = sqrt(warp_sum(sq));
     if (nrm <= eps) {
-      for (int c = 0; c < D; ++c) dx[c] = dy[c] / eps;
+      for (int c = lane; c < D; c += 32) dX[r * D + c] = dy[c] / eps;
       continue;
     }
     T dot = T(0);
-    for (int c = 0; c < D; ++c) dot += x[c] / nrm * dy[c];
-    for (int c = 0; c < D; ++c) dx[c] = (dy[c] - x[c] / nrm * dot) / nrm;
+    for (int c = lane; c < D; c += 32) dot += x[c] / nrm * dy[c];
+    dot = warp_sum(dot);
+    for (int c = lane; c < D; c += 32) dX[r * D + c] = (dy[c] - x[c] / nrm * dot) / nrm;
   }
 }
 
@@ -205,7 +214,7 @@ bool whole_graph(const DevGraph& g, const char* who) {
 template <typename T>
 int l2_launch(int64_t n, int H, int D, const T* X, T* Y, cudaStream_t s, T eps = T(1e-12)) {
   if (n == 0) return GF_OK;
-  l2_rows<T><<<grid_for(n * H), 256, 0, s>>>(n, H, D, X, Y, eps);
+  l2_rows<T><<<grid_for(n * H * 32), 256, 0, s>>>(n * H, D, X, Y, eps);
   GF_CHECK_LAUNCH("l2_rows");
   return GF_OK;
 }
@@ -214,7 +223,7 @@ template <typename T>
 int l2_bwd_launch(int64_t n, int H, int D, const T* X, const T* dY, T* dX, cudaStream_t s,
                   T eps = T(1e-12)) {
   if (n == 0) return GF_OK;
-  l2_rows_bwd<T><<<grid_for(n * H), 256, 0, s>>>(n, H, D, X, dY, dX, eps);
+  l2_rows_bwd<T><<<grid_for(n * H * 32), 256, 0, s>>>(n * H, D, X, dY, dX, eps);
   GF_CHECK_LAUNCH("l2_rows_bwd");
   return GF_OK;
 }
@@ -247,7 +256,7 @@ int sddmm_backward_impl(DevGraph& g, const gf_attn_desc& d, const T* Q, const T*
   }
   // AGNN: gradients w.r.t. the normalised rows, then through the normalisation
   T* tmp = nullptr;
-  GF_CHECK_CUDA(cudaMallocAsync(&tmp, sizeof(T) * nf * 4, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&tmp, sizeof(T) * nf * 4, s));
   T *qn = tmp, *kn = tmp + nf, *gq = tmp + 2 * nf, *gk = tmp + 3 * nf;
   int rc = l2_launch<T>(g.n, H, D, Q, qn, s);
   if (!rc) rc = l2_launch<T>(g.n, H, D, K, kn, s);
