@@ -32,6 +32,7 @@ try:
         gen_super_node,
         gradcheck,
         load_graph,
+        run_benchmark_json,
         save_graph,
         select_strategy,
         super_node_threshold,
@@ -52,6 +53,7 @@ __all__ = [
     "gen_super_node",
     "gradcheck",
     "load_graph",
+    "run_benchmark_json",
     "save_graph",
     "select_strategy",
     "super_node_threshold",
