@@ -472,6 +472,78 @@ def backward_ablation(dg, spec, Q, K, V, O, stats, dO, stream, flush, steps=5):
     return out
 
 
+def e2e_pipelined(dg, spec, tabs, stream, steps, warmup=2):
+    """End-to-end throughput through the C-ABI with HOST buffers, steps
+    pipelined over two buffer sets: every step copies ITS OWN inputs (Q|el,
+    K|er, V, dO) host->device and its outputs (O, dQ|del, dK|der, dV)
+    device->host inside the timed region, and step i+1's upload and step
+    i-1's download run on copy streams under step i's kernels (the serving
+    arrangement for independent requests).  Returns ms per step."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    ins, outs = ("Q", "K", "V", "dO"), ("O", "dQ", "dK", "dV")
+    sets = []
+    for b in range(2):
+        d = {k: torch.empty_like(v) for k, v in tabs.items()}
+        hi = {k: tabs[k].cpu().pin_memory() for k in ins}
+        ho = {k: torch.empty(tabs[k].shape, dtype=tabs[k].dtype).pin_memory() for k in outs}
+        sets.append((d, hi, ho))
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    comp_done, out_done = [None, None], [None, None]
+
+    def step(i):
+        b = i % 2
+        d, hi, ho = sets[b]
+        if comp_done[b] is not None:  # step i-2 has finished reading inputs b
+            s_in.wait_event(comp_done[b])
+        with torch.cuda.stream(s_in):
+            for k in ins:
+                d[k].copy_(hi[k], non_blocking=True)
+        ev_in = torch.cuda.Event()
+        ev_in.record(s_in)
+        stream.wait_event(ev_in)
+        if out_done[b] is not None:  # step i-2's outputs b are on the host
+            stream.wait_event(out_done[b])
+        fused.attn_forward(dg, spec, d["Q"], d["K"], d["V"], O=d["O"], stats=d["stats"],
+                           stream=stream)
+        ev_f = torch.cuda.Event()
+        ev_f.record(stream)
+        fused.attn_backward_rows(dg, spec, d["Q"], d["K"], d["V"], d["O"], d["stats"], d["dO"],
+                                 d["dK"], stream=stream)
+        fused.attn_backward_cols(dg, spec, d["Q"], d["K"], d["V"], d["stats"], d["dO"], d["dQ"],
+                                 d["dV"], stream=stream)
+        ev_c = torch.cuda.Event()
+        ev_c.record(stream)
+        comp_done[b] = ev_c
+        s_out.wait_event(ev_f)
+        with torch.cuda.stream(s_out):
+            ho["O"].copy_(d["O"], non_blocking=True)
+        s_out.wait_event(ev_c)
+        with torch.cuda.stream(s_out):
+            for k in ("dQ", "dK", "dV"):
+                ho[k].copy_(d[k], non_blocking=True)
+        ev_o = torch.cuda.Event()
+        ev_o.record(s_out)
+        out_done[b] = ev_o
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    s_in.wait_event(start)
+    s_out.wait_event(start)
+    for i in range(steps):
+        step(warmup + i)
+    for ev in out_done:
+        stream.wait_event(ev)
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end) / steps
+
+
 def run_ours(args, rank, world):
     import numpy as np
     import torch
@@ -588,7 +660,7 @@ def run_ours(args, rank, world):
     value = e * args.steps / (sum_ms / 1e3) / 1e9
 
     # ---- e2e through the C-ABI with pinned host buffers
-    e2e_val, h2d, d2h = None, 0, 0
+    e2e_val, e2e_serial, h2d, d2h = None, None, 0, 0
     if not sharded:
         hQ, hK, hV, hdO = [x.cpu().pin_memory() for x in (Q, K, V, dO)]
         hO, hdQ, hdK, hdV = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (O, dQ, dK, dV)]
@@ -642,7 +714,11 @@ def run_ours(args, rank, world):
             b.record(stream)
             b.synchronize()
             ee.append(a.elapsed_time(b))
-        e2e_val = e / (statistics.mean(ee) / 1e3) / 1e9
+        e2e_serial = e / (statistics.mean(ee) / 1e3) / 1e9
+        tabs = {"Q": Q, "K": K, "V": V, "dO": dO, "O": O, "stats": stats, "dQ": dQ, "dK": dK,
+                "dV": dV}
+        e2e_ms = e2e_pipelined(dg, spec, tabs, stream, args.steps)
+        e2e_val = e / (e2e_ms / 1e3) / 1e9
 
     # ---- layer level (projections reported separately): the
     # conv_forward / conv_backward step of models.hpp:104-158 with X of width
@@ -710,7 +786,14 @@ def run_ours(args, rank, world):
                               "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "GEdges/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "mode": "pinned host buffers through the C-ABI; every step copies its own "
+                            "inputs H2D and outputs D2H inside the timed region, double-buffered "
+                            "so step i+1's upload and step i-1's download overlap step i's "
+                            "kernels; 134 MB of fresh input per step (> L2)",
+                    "serial_value": e2e_serial,
+                    "serial_mode": "one step at a time (copies overlap only within the step), "
+                                   "L2 flushed between steps"},
             "layer": layer_out,
             "fwd_strategy_ms": ablation,
             "bwd_strategy_ms": bwd_ablation,
