@@ -154,6 +154,14 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi has produced a sample (its start-up takes a
+        few hundred ms), so the timed region is covered from its start."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.first = len(self.rows)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -169,16 +177,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[max(0, getattr(self, "first", 1) - 1):]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        reasons = sorted({names[i] for r in rows for i in range(4)
                           if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def measured_peak_hbm():
@@ -188,6 +197,21 @@ def measured_peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback"
+
+
+def measured_l2_gather(row_bytes, footprint=64 << 20):
+    """Live L2 gather peak (GB/s) for rows of the hot kernels' gathered row
+    size from an L2-resident footprint (gf_measure_l2_gather; same 256-bit
+    non-coherent loads).  The second roofline denominator: the C4 node tables
+    (V 60 MB + el 7.5 MB) are L2-resident, so HBM is not the binding limit."""
+    import ctypes as C
+
+    from paper_2411_16127_b200._capi import check, lib
+
+    rb = max(32, min(1024, (row_bytes + 31) // 32 * 32))
+    g = C.c_double()
+    check(lib().gf_measure_l2_gather(footprint, rb, 5, C.byref(g), None), "gf_measure_l2_gather")
+    return g.value, rb
 
 
 def ncu_traffic(config, kernel):
@@ -285,6 +309,53 @@ def main():
     return run_ours(args, rank, world)
 
 
+# Edge fraction of the reference arm's per-step sample (a row slice; whole
+# graph for the small configs) so one `--steps 50` run stays within minutes.
+REF_SAMPLE_FRAC = {"cora": 1.0, "molhiv": 1.0, "pubmed": 1.0, "reddit": 1.0 / 16,
+                   "products": 1.0 / 64}
+
+
+def gen_graph_cpu(name, frac=1.0, seed=1):
+    """The bench graphs' shapes generated on the CPU (numpy; the reference arm
+    runs no GPU code), restricted to the destination rows [0, r) that hold
+    ~frac of the edges (node ids are random, so the slice has the graph's
+    degree mix).  Returns (n, src, dst) int64 unique edges."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    if name == "reddit":
+        n = REDDIT_N
+        deg_of = np.empty(n, np.int64)
+        deg_of[rng.permutation(n)] = reddit_degrees(np)
+        cum = np.cumsum(deg_of)
+        r = int(np.searchsorted(cum, cum[-1] * frac)) + 1
+        dst = np.repeat(np.arange(r, dtype=np.int64), deg_of[:r])
+        src = rng.integers(0, n, dst.shape[0])
+    elif name == "molhiv":
+        mols, atoms = 1024, 26
+        s_all, d_all = [], []
+        for m in range(mols):
+            base = m * atoms
+            parent = [rng.integers(0, i) for i in range(1, atoms)]
+            a = [base + i for i in range(1, atoms)] + [base + x for x in rng.integers(0, atoms, 3)]
+            b = [base + p for p in parent] + [base + x for x in rng.integers(0, atoms, 3)]
+            s_all += a + b
+            d_all += b + a
+        n = mols * atoms
+        src, dst = np.array(s_all, np.int64), np.array(d_all, np.int64)
+        keep = src != dst
+        src, dst = src[keep], dst[keep]
+    else:
+        n, e = {"cora": (2_708, 10_556), "pubmed": (19_717, 88_648),
+                "products": (2_400_000, 62_000_000)}[name]
+        r = max(1, int(round(n * frac)))
+        e_s = int(round(e * r / n))
+        src = rng.integers(0, n, e_s)
+        dst = rng.integers(0, r, e_s)
+    key = np.unique(dst * n + src)
+    return n, key % n, key // n
+
+
 def run_reference(args, rank, world):
     """The reference's own CPU path (oracle/_ref), rank 0 only, on a bounded
     sample of the same workload per step."""
@@ -293,25 +364,11 @@ def run_reference(args, rank, world):
     graph, layer, H, D, desc = CONFIGS[args.config]
     if rank != 0:
         return 0
-    if graph != "reddit":
-        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for c4"}))
-        return 0
-    # Sample: the first rows by id holding ~1/16 of the edges, generated on the
-    # CPU from the same degree sequence (the reference arm uses no GPU code).
-    rng = np.random.default_rng(1)
-    deg = reddit_degrees(np)
-    perm = rng.permutation(REDDIT_N)
-    deg_of = np.empty(REDDIT_N, np.int64)
-    deg_of[perm] = deg
-    frac = 1.0 / 16
-    cum = np.cumsum(deg_of)
-    r = int(np.searchsorted(cum, cum[-1] * frac)) + 1
-    dst = np.repeat(np.arange(r, dtype=np.int64), deg_of[:r])
-    src = rng.integers(0, REDDIT_N, dst.shape[0])
-    key = np.unique(dst * REDDIT_N + src)
     import oracle
 
-    sub = oracle.from_coo(REDDIT_N, key % REDDIT_N, key // REDDIT_N)
+    frac = REF_SAMPLE_FRAC[graph]
+    n, src, dst = gen_graph_cpu(graph, frac)
+    sub = oracle.from_coo(n, src, dst)
     times, es = cpu_reference_sample(sub, layer, D, steps=args.warmup + args.steps)
     t = times[args.warmup:]
     per_step = sum(t) / len(t) * H  # one call per head, H heads
@@ -321,12 +378,14 @@ def run_reference(args, rank, world):
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "sample_edges": es, "sample": "1 head x row slice (1/16 of edges), x8 heads"},
+        "config": {"workload": desc, "sample_edges": es,
+                   "sample": f"1 head x row slice ({frac:g} of the edges), x{H} heads"},
         "cpu_baseline": {"value": value, "unit": "GEdges/s", "cores": os.cpu_count(),
                          "kind": "reference",
                          "sample": f"reference run_strategy<float>+fused_backward<float>, 1 of {H} "
-                                   f"heads on a {es}-edge row slice of the C4 graph; fwd uses all "
-                                   "hardware threads, bwd is single-threaded by construction"},
+                                   f"heads on a {es}-edge row slice ({frac:g} of E) of a CPU-generated "
+                                   f"{graph}-shape graph; fwd uses all hardware threads, bwd is "
+                                   "single-threaded by construction"},
         "e2e": {"value": value, "unit": "GEdges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -634,6 +693,7 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NEV)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        clk.wait_first()
         if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -745,6 +805,7 @@ def run_ours(args, rank, world):
     peak, peak_kind = measured_peak_hbm()
     traffic = ncu_traffic(args.config, dom)
     step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D) for k in means)
+    l2_peak, l2_rb = measured_l2_gather(F * 4)
 
     cpu = None
     if need_cpu:
@@ -781,6 +842,11 @@ def run_ours(args, rank, world):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes": ab},
+            "l2_roofline": {"bound": "l2", "kernel": dom, "achieved": achieved, "peak": l2_peak,
+                            "unit": "GB/s", "frac": achieved / l2_peak,
+                            "step_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / l2_peak,
+                            "peak_kind": f"measured live: gf_measure_l2_gather, {l2_rb} B rows "
+                                         "(the gathered row size), 64 MiB L2-resident footprint"},
             "step_roofline": {"algorithmic_bytes": step_bytes,
                               "achieved": step_bytes / (ms_per_step / 1e3) / 1e9,
                               "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},

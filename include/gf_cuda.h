@@ -233,6 +233,14 @@ int gf_gat_fanin(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf,
                  const void* a_r, const void* dV, const void* del, const void* der, void* dH,
                  void* da_l, void* da_r, void* stream);
 
+/* ---- diagnostics ----
+ * Measured gather bandwidth (GB/s) of rows of row_bytes (32..1024, lanes read
+ * consecutive 32 B chunks with 256-bit non-coherent loads) chosen in hashed
+ * order from a footprint_bytes buffer, every SM, after a warm-up pass: with
+ * an L2-resident footprint, the roofline denominator for the gather kernels. */
+int gf_measure_l2_gather(size_t footprint_bytes, int32_t row_bytes, int32_t iters,
+                         double* gbs_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

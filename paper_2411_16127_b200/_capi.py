@@ -74,6 +74,8 @@ SIGNATURES = {
                                    _vp]),
     "gf_softmax_backward": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
     "gf_sddmm_backward": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gf_measure_l2_gather": (C.c_int, [C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                       _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp]),
     "gf_attn_bwd_rows": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,

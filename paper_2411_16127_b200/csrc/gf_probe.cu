@@ -1,0 +1,78 @@
+// Measured L2 gather bandwidth: the denominator for the gather kernels whose
+// node tables are L2-resident (C4: V 60 MB + el 7.5 MB), where the HBM
+// roofline is exceeded by design (SURVEY §7 hard part 5).  Same instruction
+// as the hot kernels' gathers (LDG.E.256 non-coherent, L1 no-allocate, L2
+// evict-last), rows of `row_bytes` of a `footprint`-byte buffer in a hashed
+// order, all SMs, after one warm-up pass.
+#include <algorithm>
+
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+
+namespace gfb {
+namespace {
+
+// Lanes in groups of `cpr` (chunks per row) read the consecutive 32 B chunks
+// of one randomly chosen row, like the hot kernels' per-edge row gathers
+// (GAT 8x8: 8 lanes x 32 B = one 256 B V row).
+__global__ void __launch_bounds__(256) l2_gather_probe(const float* __restrict__ buf,
+                                                       uint32_t rows, uint32_t cpr,
+                                                       uint32_t per_thread,
+                                                       float* __restrict__ sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t grp = tid / cpr, sub = tid % cpr;
+  float acc = 0.f;
+  uint32_t x = grp * 2654435761u + 12345u;
+#pragma unroll 4
+  for (uint32_t i = 0; i < per_thread; ++i) {
+    x = x * 1664525u + 1013904223u;  // the group's LCG walk over the rows
+    float v[8];
+    ld_gather<float, 32>(buf + (static_cast<size_t>(x % rows) * cpr + sub) * 8, v);
+    acc += v[0] + v[7];
+  }
+  if (acc == 12345.678f) sink[tid] = acc;  // keeps the loads alive
+}
+
+}  // namespace
+}  // namespace gfb
+
+extern "C" int gf_measure_l2_gather(size_t footprint_bytes, int32_t row_bytes, int32_t iters,
+                                    double* gbs_out, void* stream) {
+  if (!gbs_out || footprint_bytes < 32 || iters < 1 || row_bytes < 32 || row_bytes % 32 ||
+      row_bytes > 1024 || (32 % (row_bytes / 32) && (row_bytes / 32) % 32)) {
+    gfb::set_error("gf_measure_l2_gather: invalid arguments");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  const uint32_t cpr = static_cast<uint32_t>(row_bytes / 32);
+  const uint32_t rows = static_cast<uint32_t>(footprint_bytes / row_bytes);
+  const uint32_t chunks = rows * cpr;
+  const int blocks = 148 * 8, threads = 256;
+  const uint32_t per_thread = 1024;
+  float *buf = nullptr, *sink = nullptr;
+  GF_CHECK_CUDA(cudaMalloc(&buf, static_cast<size_t>(chunks) * 32));
+  GF_CHECK_CUDA(cudaMalloc(&sink, sizeof(float) * blocks * threads));
+  cudaMemsetAsync(buf, 0, static_cast<size_t>(chunks) * 32, s);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  gfb::l2_gather_probe<<<blocks, threads, 0, s>>>(buf, rows, cpr, per_thread, sink);  // warm L2
+  cudaEventRecord(a, s);
+  for (int i = 0; i < iters; ++i)
+    gfb::l2_gather_probe<<<blocks, threads, 0, s>>>(buf, rows, cpr, per_thread, sink);
+  cudaEventRecord(b, s);
+  int rc = GF_OK;
+  if (cudaEventSynchronize(b) != cudaSuccess) {
+    gfb::set_error("gf_measure_l2_gather: kernel failed");
+    rc = GF_ERR_CUDA;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  const double bytes = 32.0 * blocks * threads * static_cast<double>(per_thread) * iters;
+  *gbs_out = ms > 0 ? bytes / (ms * 1e-3) / 1e9 : 0.0;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(sink);
+  return rc;
+}
