@@ -84,6 +84,9 @@ typedef struct gf_graph_info {
   int32_t n_cta_cols;      /* CSC columns in the CTA bucket */
   int32_t n_empty_cols;
   int32_t device;
+  int32_t n_small_rows;    /* CSR rows of degree 1..8: packed several per warp, one lane group
+                              each (just before the empty rows in the order) */
+  int32_t n_small_cols;
 } gf_graph_info;
 
 const char* gf_last_error(void);

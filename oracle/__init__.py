@@ -52,7 +52,7 @@ def lib():
         _ora.gfo_from_coo.restype = C.c_int
         _ora.gfo_from_coo.argtypes = [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         _ora.gfo_schedule.restype = None
-        _ora.gfo_schedule.argtypes = [C.c_int64, _vp, C.c_int64, _vp, _vp, _vp]
+        _ora.gfo_schedule.argtypes = [C.c_int64, _vp, C.c_int64, _vp, _vp, _vp, _vp]
         for sfx in ("f32", "f64"):
             f = getattr(_ora, "gfo_forward_" + sfx)
             f.restype = C.c_int
@@ -163,12 +163,15 @@ def from_coo(n, src, dst) -> CSR:
     return CSR(n, rp, col[:e], cp, cr[:e], perm[:e])
 
 
-def schedule(n, ptr, cta_threshold):
+def schedule(n, ptr, cta_threshold, want_small=False):
     order = np.zeros(max(n, 1), np.int32)
     nc = np.zeros(1, np.int64)
     nz = np.zeros(1, np.int64)
+    ns = np.zeros(1, np.int64)
     lib().gfo_schedule(n, _ptr(np.ascontiguousarray(ptr, np.int64)), cta_threshold, _ptr(order),
-                       _ptr(nc), _ptr(nz))
+                       _ptr(nc), _ptr(nz), _ptr(ns))
+    if want_small:
+        return order[:n], int(nc[0]), int(nz[0]), int(ns[0])
     return order[:n], int(nc[0]), int(nz[0])
 
 

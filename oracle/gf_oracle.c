@@ -62,7 +62,7 @@ int gfo_from_coo(int64_t n, int64_t e, const int64_t* src, const int64_t* dst, i
 /* ------------------------------------------------------------- schedule -- */
 
 void gfo_schedule(int64_t n, const int64_t* ptr, int64_t cta_threshold, int32_t* order,
-                  int64_t* n_cta, int64_t* n_empty) {
+                  int64_t* n_cta, int64_t* n_empty, int64_t* n_small) {
   /* Stable sort by degree descending = counting sort over distinct degrees.
    * Degrees are bounded by E, so use a sort on (deg desc, row asc) pairs via
    * a simple merge sort of row indices keyed by degree. */
@@ -84,15 +84,17 @@ void gfo_schedule(int64_t n, const int64_t* ptr, int64_t cta_threshold, int32_t*
     idx = buf;
     buf = t;
   }
-  int64_t c = 0, z = 0;
+  int64_t c = 0, z = 0, sm = 0;
   for (int64_t i = 0; i < n; ++i) {
     order[i] = (int32_t)idx[i];
     int64_t d = ptr[idx[i] + 1] - ptr[idx[i]];
     if (d >= cta_threshold && d > 0) ++c;
     if (d == 0) ++z;
+    if (d >= 1 && d <= GFO_SMALL_DEGREE && d < cta_threshold) ++sm;
   }
   *n_cta = c;
   *n_empty = z;
+  if (n_small) *n_small = sm;
   free(idx);
   free(buf);
 }

@@ -32,9 +32,11 @@ int gfo_from_coo(int64_t n, int64_t e, const int64_t* src, const int64_t* dst, i
  * scheduler's definition so the device schedule can be checked bit-exactly).
  * order = rows stably sorted by degree descending; n_cta = #rows with
  * degree >= cta_threshold (they lead the order); n_empty = #rows of degree 0
- * (they trail it). */
+ * (they trail it); n_small = #rows of degree 1..GFO_SMALL_DEGREE below the
+ * CTA threshold (just before the empty ones). */
+#define GFO_SMALL_DEGREE 8 /* rows of degree 1..8 form the packed (sub-warp) bucket */
 void gfo_schedule(int64_t n, const int64_t* ptr, int64_t cta_threshold, int32_t* order,
-                  int64_t* n_cta, int64_t* n_empty);
+                  int64_t* n_cta, int64_t* n_empty, int64_t* n_small);
 
 /* engine.hpp:192-231 (run_block_rows) + kernels.hpp:50-61 (l2_normalize_rows)
  * per head.  variant: 0 dot, 1 add. */

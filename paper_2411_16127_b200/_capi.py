@@ -33,7 +33,8 @@ class GraphInfo(C.Structure):
                 ("max_in_degree", C.c_int64), ("max_out_degree", C.c_int64),
                 ("cta_threshold", C.c_int32), ("n_cta_rows", C.c_int32),
                 ("n_empty_rows", C.c_int32), ("n_cta_cols", C.c_int32),
-                ("n_empty_cols", C.c_int32), ("device", C.c_int32)]
+                ("n_empty_cols", C.c_int32), ("device", C.c_int32),
+                ("n_small_rows", C.c_int32), ("n_small_cols", C.c_int32)]
 
 
 # Every symbol include/gf_cuda.h declares, with its ctypes signature.

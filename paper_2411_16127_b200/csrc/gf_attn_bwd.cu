@@ -81,25 +81,18 @@ __device__ __forceinline__ void warp_sum(T (&x)[NV]) {
 }
 
 // ------------------------------------------------------------ pass A ------
-template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
+template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
+__device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, const int warp,
+                                        const bool cta, const int slot, const bool live) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
   constexpr int U = CPL == 1 ? GF_U_ROWS : GF_U2;
   constexpr int NA = VAR == GF_DOT ? NE : 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  int slot;
-  if (cta) {
-    slot = blockIdx.x;
-  } else {
-    slot = a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
-    if (slot >= a.n) return;
-  }
-  const int v = __ldg(a.order + slot);
-  int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
+  const int v = live ? __ldg(a.order + slot) : 0;
+  int eb = live ? __ldg(a.ptr + v) : 0, ee = live ? __ldg(a.ptr + v + 1) : 0;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
 
   const int h = c / a.LPH;
@@ -140,20 +133,23 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_r
 #pragma unroll
   for (int j = 0; j < NA; ++j) acc[j] = T(0);
 
-  int nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
-  for (int base = eb; base < ee; base += 32) {
-    const int cnt = min(32, ee - base);
+  constexpr int ep = pk ? 1 : EPW;
+  const int js = pk ? 0 : sub;
+  int nxt = !pk && eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
+  for (int base = eb; pk || base < ee; base += 32) {
+    const int cnt = pk ? ee - eb : min(32, ee - base);
+    const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
     const int myu = nxt;
-    nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
+    if (!pk) nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
+    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
       bool ok[U];
       T vv[U][NE], qv[U][NE], el[U];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * EPW + sub;
+        const int j = j0 + t * ep + js;
         ok[t] = j < cnt;
-        const int u = __shfl_sync(kFull, myu, j & 31);
+        const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
         const int uu = ok[t] ? u : 0;
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
@@ -201,45 +197,62 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_r
         }
       }
     }
+    if (pk) break;
   }
 
-  warp_sum<T, LPE, NA>(acc);
+  if (!pk) warp_sum<T, LPE, NA>(acc);
   if (cta && !cta_sum<T, LPE, NA>(acc, warp, c, sub)) return;
+  const bool writer = pk ? live : sub == 0;
 
   if constexpr (VAR == GF_DOT) {
     if (a.l2) l2_backward_row<T, NE>(acc, kv, a.LPH);
-    if (sub == 0) {
+    if (writer) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k)
         st_chunk<T, CB>(a.dK + vrow + k * CW, *reinterpret_cast<T(*)[CW]>(acc + k * CW));
     }
   }
-  if (sub == 0 && c % a.LPH == 0) {
+  if (writer && c % a.LPH == 0) {
     a.stats[4 * ri + 3] = delta;
     if constexpr (VAR == GF_ADD) a.dK[ri] = acc[0];
   }
 }
 
-// ------------------------------------------------------------ pass B ------
+// Bucket dispatch shared by both passes: CTA rows, warp rows, packed rows.
+#define GF_BWD_DISPATCH(ROWFN)                                                                  \
+  constexpr int EPW = 32 / LPE;                                                                 \
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;                                   \
+  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);                                 \
+  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {                         \
+    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp; \
+    if (!cta && slot >= a.pk0) return;                                                          \
+    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true);                         \
+  } else if constexpr (EPW > 1) {                                                               \
+    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW + \
+                     lane / LPE;                                                                \
+    const bool live = slot < a.n;                                                               \
+    if (!__any_sync(kFull, live)) return;                                                       \
+    ROWFN<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live);                        \
+  }
+
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
+  GF_BWD_DISPATCH(bwd_row)
+}
+
+// ------------------------------------------------------------ pass B ------
+template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
+__device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, const int warp,
+                                        const bool cta, const int slot, const bool live) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
   constexpr int U = CPL == 1 ? GF_U_COLS : GF_U2;
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr bool pk = PK;  // packed column: this LPE-lane group owns the column
   const int c = lane % LPE, sub = lane / LPE;
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  int slot;
-  if (cta) {
-    slot = blockIdx.x;
-  } else {
-    slot = a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
-    if (slot >= a.n) return;
-  }
-  const int u = __ldg(a.order + slot);
-  int sb = __ldg(a.ptr + u), se = __ldg(a.ptr + u + 1);
+  const int u = live ? __ldg(a.order + slot) : 0;
+  int sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
   if (cta) split_range(sb, se, kWarpsPerBlock, warp, sb, se);
 
   const int h = c / a.LPH;
@@ -273,21 +286,24 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
 #pragma unroll
   for (int j = 0; j < NT; ++j) all[j] = T(0);
 
-  int nxt = sb + lane < se ? ld_idx(a.idx + sb + lane) : 0;
-  for (int base = sb; base < se; base += 32) {
-    const int cnt = min(32, se - base);
+  constexpr int ep = pk ? 1 : EPW;
+  const int js = pk ? 0 : sub;
+  int nxt = !pk && sb + lane < se ? ld_idx(a.idx + sb + lane) : 0;
+  for (int base = sb; pk || base < se; base += 32) {
+    const int cnt = pk ? se - sb : min(32, se - base);
+    const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
     const int myv = nxt;
-    nxt = base + 32 + lane < se ? ld_idx(a.idx + base + 32 + lane) : 0;
+    if (!pk) nxt = base + 32 + lane < se ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
+    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
       bool ok[U];
       T dov[U][NE], kv[U][NE];
       Rec<T> rec[U];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * EPW + sub;
+        const int j = j0 + t * ep + js;
         ok[t] = j < cnt;
-        const int v = __shfl_sync(kFull, myv, j & 31);
+        const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
         const int vv = ok[t] ? v : 0;
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
@@ -333,9 +349,10 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
         }
       }
     }
+    if (pk) break;
   }
 
-  warp_sum<T, LPE, NT>(all);
+  if (!pk) warp_sum<T, LPE, NT>(all);
   if (cta && !cta_sum<T, LPE, NT>(all, warp, c, sub)) return;
 
   T g[NE];
@@ -344,7 +361,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
     for (int i = 0; i < NE; ++i) g[i] = all[NE + i];
     if (a.l2) l2_backward_row<T, NE>(g, qu, a.LPH);
   }
-  if (sub == 0) {
+  if (pk ? live : sub == 0) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       st_chunk<T, CB>(a.dV + urow + k * CW, *reinterpret_cast<T(*)[CW]>(all + k * CW));
@@ -355,6 +372,11 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
       if (c % a.LPH == 0) a.dQ[static_cast<size_t>(u) * a.H + h] = all[NE];
     }
   }
+}
+
+template <typename T, int CB, int LPE, int CPL, int VAR>
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
+  GF_BWD_DISPATCH(bwd_col)
 }
 
 // ----------------------------------------------------------- generic path --
@@ -581,8 +603,17 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   const bool fast_b = base && aligned(a.V, 16) && aligned(a.dO, cb) && aligned(a.dV, 16) &&
                       (!dot || (aligned(a.Q, 16) && aligned(a.K, cb) && aligned(a.dQ, 16)));
   ra.LPH = ca.LPH = fs.ok ? fs.lph : 1;
-  const int rb = (do_a && fast_a) ? ra.n_cta + (ra.n - ra.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
-  const int cbk = (do_b && fast_b) ? ca.n_cta + (ca.n - ca.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+  // bucket geometry (see fwd): warp bucket [n_cta, pk0), packed [pk0, n)
+  const int epw = fs.ok ? 32 / fs.lpe : 1;
+  auto buckets = [&](BwdArgs<T>& x, int n_small, int n_empty) {
+    x.pk0 = epw > 1 ? std::max(x.n_cta, g.n - n_empty - n_small) : x.n;
+    x.pk0 = std::min(x.pk0, x.n);
+    x.wblocks = (x.pk0 - x.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int per_block = kWarpsPerBlock * epw;
+    return x.n_cta + x.wblocks + (x.n - x.pk0 + per_block - 1) / per_block;
+  };
+  const int rb = (do_a && fast_a) ? buckets(ra, g.n_small_rows, g.n_empty_rows) : 0;
+  const int cbk = (do_b && fast_b) ? buckets(ca, g.n_small_cols, g.n_empty_cols) : 0;
   if (rb || cbk) {
     int rc = GF_OK;
     switch (fs.cb * 1000 + fs.lpe * 10 + fs.cpl) {

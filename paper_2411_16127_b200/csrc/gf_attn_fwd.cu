@@ -40,24 +40,18 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
 // MODE 0: SMMF (scores computed here); 1: PMF's fused softmax + SpMM over the
 // scores an edge-parallel SDDMM wrote to a.ES; 2: the unfused SpMM (a.ES holds
 // normalised probabilities: O = sum p V, no softmax, no records).
-template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
+// One row (CTA slice, warp row, or — PK — one packed row per LPE-lane group).
+template <typename T, int CB, int LPE, int CPL, int VAR, int MODE, bool PK>
+__device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, const int warp,
+                                        const bool cta, const int slot, const bool live) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
   constexpr int U = CPL == 1 ? GF_U_FWD : GF_U2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPE, sub = lane / LPE;
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  int slot;
-  if (cta) {
-    slot = blockIdx.x;
-  } else {
-    slot = a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
-    if (slot >= a.n) return;
-  }
-  const int v = __ldg(a.order + slot);
-  int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
+  constexpr bool pk = PK;
+  const int v = live ? __ldg(a.order + slot) : 0;
+  int eb = live ? __ldg(a.ptr + v) : 0, ee = live ? __ldg(a.ptr + v + 1) : 0;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
 
   const int h = c / a.LPH;
@@ -93,20 +87,26 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
 #pragma unroll
   for (int i = 0; i < NE; ++i) acc[i] = T(0);
 
-  int nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
-  for (int base = eb; base < ee; base += 32) {
-    const int cnt = min(32, ee - base);
+  // Warp / CTA rows: 32 ids per chunk, one per lane, shuffled to the edge
+  // slots (next chunk prefetched); packed rows: each group walks its own
+  // <= kSmallDegree edges one per step, loading ids directly.
+  constexpr int ep = pk ? 1 : EPW;
+  const int js = pk ? 0 : sub;
+  int nxt = !pk && eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
+  for (int base = eb; pk || base < ee; base += 32) {
+    const int cnt = pk ? ee - eb : min(32, ee - base);
+    const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
     const int myu = nxt;  // ids of this 32-edge chunk; prefetch the next one
-    nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
+    if (!pk) nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
 #pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += EPW * U) {
+    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
       bool ok[U];
       T vv[U][NE], qv[U][NE], s[U];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * EPW + sub;
+        const int j = j0 + t * ep + js;
         ok[t] = j < cnt;
-        const int u = __shfl_sync(kFull, myu, j & 31);
+        const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
         const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
@@ -169,12 +169,13 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
         for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
       }
     }
+    if (pk) break;
   }
 
   // Merge the EPW edge slots of the warp (butterfly: every lane ends with
-  // the warp's state).
+  // the warp's state); packed groups each own a row and skip it.
 #pragma unroll
-  for (int o = LPE; o < 32; o <<= 1) {
+  for (int o = LPE; o < (pk ? LPE : 32); o <<= 1) {
     T acc2[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) acc2[i] = __shfl_xor_sync(kFull, acc[i], o);
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
     __syncthreads();
     if (warp != 0) return;
     if (sub == 0) {
-      const T* d0 = sm[0][c];
+      const T* d0 = sm[0][c];  // (CTA rows are never packed)
       m = d0[0];
       l = d0[1];
 #pragma unroll
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
     }
   }
 
-  if (sub == 0) {
+  if (pk ? live : sub == 0) {
     const T r = MODE >= 2 ? a.scale : (l == T(0) ? T(0) : T(1) / l);
     T o[NE];
 #pragma unroll
@@ -236,6 +237,27 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
       rec[1] = l == T(0) ? T(0) : lg2(l);
       rec[2] = VAR == GF_DOT ? rk : erv;
     }
+  }
+}
+
+// Three buckets (degree-descending order): CTA rows (edge-split over 8
+// warps), warp rows, and packed rows (degree <= kSmallDegree, EPW rows per
+// warp, one LPE-lane group each); the bucket is warp-uniform.
+template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
+__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
+  constexpr int EPW = 32 / LPE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
+  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
+    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
+    if (!cta && slot >= a.pk0) return;
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, cta, slot, true);
+  } else if constexpr (EPW > 1) {
+    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW +
+                     lane / LPE;
+    const bool live = slot < a.n;
+    if (!__any_sync(kFull, live)) return;
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, true>(a, lane, warp, false, slot, live);
   }
 }
 
@@ -401,8 +423,14 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
                   (mode >= 2 || variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
   if (al) {
     a.LPH = fs.lph;
-    const int warp_rows = a.n - a.n_cta;
-    const int blocks = a.n_cta + (warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int epw = 32 / fs.lpe;
+    // packed bucket: the small rows (and, unless skipped, the empty ones) when
+    // a warp holds more than one edge slot
+    a.pk0 = epw > 1 ? std::max(a.n_cta, g.n - g.n_empty_rows - g.n_small_rows) : a.n;
+    a.pk0 = std::min(a.pk0, a.n);
+    a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int rows_per_block = kWarpsPerBlock * epw;
+    const int blocks = a.n_cta + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;
     const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;
     switch (key) {
       case 32011: return launch_fast_fwd<T, 32, 1, 1>(a, variant, mode, blocks, s);

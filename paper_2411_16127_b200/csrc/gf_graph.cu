@@ -32,25 +32,29 @@ __global__ void degrees_kernel(const int32_t* __restrict__ ptr, int n, int32_t* 
   }
 }
 
-// stats[0] = max degree, stats[1] = #(deg >= thr), stats[2] = #(deg == 0)
+// stats[0] = max degree, stats[1] = #(deg >= thr), stats[2] = #(deg == 0),
+// stats[3] = #(1 <= deg <= kSmallDegree, deg < thr)
 __global__ void degree_stats_kernel(const int32_t* __restrict__ deg, int n, int thr,
                                     int32_t* __restrict__ stats) {
-  int mx = 0, big = 0, zero = 0;
+  int mx = 0, big = 0, zero = 0, small = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int d = deg[i];
     mx = max(mx, d);
     big += (d >= thr && d > 0);
     zero += (d == 0);
+    small += (d >= 1 && d <= kSmallDegree && d < thr);
   }
   for (int o = 16; o; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(kFull, mx, o));
     big += __shfl_xor_sync(kFull, big, o);
     zero += __shfl_xor_sync(kFull, zero, o);
+    small += __shfl_xor_sync(kFull, small, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMax(stats + 0, mx);
     atomicAdd(stats + 1, big);
     atomicAdd(stats + 2, zero);
+    atomicAdd(stats + 3, small);
   }
 }
 
@@ -62,9 +66,9 @@ int bits_for(long long x) {
 
 // Degree-descending stable order of [0, n) for a pointer array.
 int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32_t& n_cta,
-                   int32_t& n_empty, int64_t& max_deg, cudaStream_t s) {
+                   int32_t& n_empty, int32_t& n_small, int64_t& max_deg, cudaStream_t s) {
   if (n == 0) {
-    n_cta = n_empty = 0;
+    n_cta = n_empty = n_small = 0;
     max_deg = 0;
     return GF_OK;
   }
@@ -84,6 +88,7 @@ int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32
   max_deg = h[0];
   n_cta = h[1];
   n_empty = h[2];
+  n_small = h[3];
   const int end_bit = bits_for(h[0]);
   size_t tmp_bytes = 0;
   GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted,
@@ -108,10 +113,10 @@ int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
   GF_CHECK_CUDA(cudaMalloc(&g->row_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));
   GF_CHECK_CUDA(cudaMalloc(&g->col_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));
   int rc = build_schedule(g->row_ptr, g->n, g->cta_threshold, g->row_order, g->n_cta_rows,
-                          g->n_empty_rows, g->max_in, s);
+                          g->n_empty_rows, g->n_small_rows, g->max_in, s);
   if (rc) return rc;
   return build_schedule(g->csc_ptr, g->n, g->cta_threshold, g->col_order, g->n_cta_cols,
-                        g->n_empty_cols, g->max_out, s);
+                        g->n_empty_cols, g->n_small_cols, g->max_out, s);
 }
 
 void free_graph(DevGraph* g) {
@@ -296,6 +301,8 @@ extern "C" int gf_graph_get_info(gf_graph_t g, gf_graph_info* info) {
   info->n_cta_cols = g->n_cta_cols;
   info->n_empty_cols = g->n_empty_cols;
   info->device = g->device;
+  info->n_small_rows = g->n_small_rows;
+  info->n_small_cols = g->n_small_cols;
   return GF_OK;
 }
 

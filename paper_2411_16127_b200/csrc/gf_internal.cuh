@@ -60,6 +60,10 @@ struct DevGraph {
   int32_t cta_threshold = 0;
   int32_t n_cta_rows = 0, n_empty_rows = 0;
   int32_t n_cta_cols = 0, n_empty_cols = 0;
+  // rows / columns with 1 <= degree <= kSmallDegree: they sit just before the
+  // empty ones in the order and are packed several per warp (one lane group
+  // each) by the fast kernels
+  int32_t n_small_rows = 0, n_small_cols = 0;
   int64_t max_in = 0, max_out = 0;
   int device = 0;
   int32_t* coo_dst = nullptr;   // CSR-order destination per edge (built on first use by
@@ -105,6 +109,7 @@ struct DevGraph {
 #endif
 
 constexpr int kDefaultCtaThreshold = 1024;
+constexpr int kSmallDegree = 8;  // packed (sub-warp) bucket: degree 1..8
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
 
 // ---------------------------------------------------------- kernel params --
@@ -124,6 +129,7 @@ struct FwdArgs {
   const T* V;
   T* O;
   T* stats;  // N x H x 4 records (gf_device.cuh Rec)
+  int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
   const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
   const int32_t* eperm = nullptr;  // MODE 3: slot -> CSR edge id of ES (CSC passes)
 };
@@ -146,6 +152,7 @@ struct BwdArgs {
   T* dQ;     // pass B (dot) / del (add)
   T* dK;     // pass A (dot) / der (add)
   T* dV;     // pass B
+  int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
 };
 
 // Launchers (defined in gf_attn_fwd.cu / gf_attn_bwd.cu).

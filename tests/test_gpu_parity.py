@@ -194,11 +194,11 @@ def test_schedule_bit_exact(cuda):
                                                  cta_threshold=thr)
             ro, co = dg.schedule()
             t = dg.info.cta_threshold
-            er, nc, nz = oracle.schedule(g.n, g.row_ptr, t)
-            ec, ncc, nzc = oracle.schedule(g.n, g.csc_ptr, t)
+            er, nc, nz, ns = oracle.schedule(g.n, g.row_ptr, t, want_small=True)
+            ec, ncc, nzc, nsc = oracle.schedule(g.n, g.csc_ptr, t, want_small=True)
             assert np.array_equal(ro, er) and np.array_equal(co, ec), name
-            assert (dg.info.n_cta_rows, dg.info.n_empty_rows) == (nc, nz)
-            assert (dg.info.n_cta_cols, dg.info.n_empty_cols) == (ncc, nzc)
+            assert (dg.info.n_cta_rows, dg.info.n_empty_rows, dg.info.n_small_rows) == (nc, nz, ns)
+            assert (dg.info.n_cta_cols, dg.info.n_empty_cols, dg.info.n_small_cols) == (ncc, nzc, nsc)
             assert dg.info.max_in_degree == int(np.diff(g.row_ptr).max())
 
 
