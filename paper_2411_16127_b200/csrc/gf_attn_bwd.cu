@@ -91,8 +91,9 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
-  const int v = live ? __ldg(a.order + slot) : 0;
-  int eb = live ? __ldg(a.ptr + v) : 0, ee = live ? __ldg(a.ptr + v + 1) : 0;
+  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
+  const int v = rs.x;
+  int eb = rs.y, ee = rs.z;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
 
   const int h = c / a.LPH;
@@ -251,8 +252,9 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
   constexpr bool pk = PK;  // packed column: this LPE-lane group owns the column
   const int c = lane % LPE, sub = lane / LPE;
-  const int u = live ? __ldg(a.order + slot) : 0;
-  int sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
+  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
+  const int u = rs.x;
+  int sb = rs.y, se = rs.z;
   if (cta) split_range(sb, se, kWarpsPerBlock, warp, sb, se);
 
   const int h = c / a.LPH;
@@ -588,6 +590,7 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   BwdArgs<T> ra = a, ca = a;
   ra.ptr = g.row_ptr, ra.idx = g.col, ra.order = g.row_order, ra.n_cta = g.n_cta_rows;
   ca.ptr = g.csc_ptr, ca.idx = g.csc_row, ca.order = g.col_order, ca.n_cta = g.n_cta_cols;
+  ra.sched = g.row_sched, ca.sched = g.col_sched;
   ra.n = g.active_rows();
   ca.n = g.active_cols();
   const bool do_a = passes & 1, do_b = passes & 2;

@@ -50,8 +50,9 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   constexpr int U = CPL == 1 ? GF_U_FWD : GF_U2;
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
-  const int v = live ? __ldg(a.order + slot) : 0;
-  int eb = live ? __ldg(a.ptr + v) : 0, ee = live ? __ldg(a.ptr + v + 1) : 0;
+  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
+  const int v = rs.x;
+  int eb = rs.y, ee = rs.z;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
 
   const int h = c / a.LPH;

@@ -94,6 +94,7 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
   a.ptr = g.row_ptr;
   a.idx = g.col;
   a.order = g.row_order;
+  a.sched = g.row_sched;
   a.n = g.active_rows();
   a.n_cta = g.n_cta_rows;
   a.H = d.heads;

@@ -63,6 +63,15 @@ __device__ __forceinline__ T ld_edge(const T* __restrict__ p) {
   return v;
 }
 
+/// Schedule slot {node, begin, end, 0} (streamed, read once per pass).
+__device__ __forceinline__ int4 ld_sched(const int4* __restrict__ p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol_stream()));
+  return v;
+}
+
 /// Gathered scalar of a node table (el[src], ...).
 template <typename T>
 __device__ __forceinline__ T ld_node(const T* __restrict__ p) {

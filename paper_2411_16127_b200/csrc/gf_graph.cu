@@ -107,6 +107,22 @@ int build_schedule(const int32_t* d_ptr, int n, int thr, int32_t* d_order, int32
   return GF_OK;
 }
 
+__global__ void sched_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ ptr,
+                             int n, int4* __restrict__ sched) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = order[i];
+    sched[i] = make_int4(v, ptr[v], ptr[v + 1], 0);
+  }
+}
+
+int build_sched(const int32_t* order, const int32_t* ptr, int n, int4** out, cudaStream_t s) {
+  GF_CHECK_CUDA(cudaMalloc(out, sizeof(int4) * (n > 0 ? n : 1)));
+  if (n == 0) return GF_OK;
+  sched_kernel<<<std::min(4096, (n + 255) / 256), 256, 0, s>>>(order, ptr, n, *out);
+  GF_CHECK_LAUNCH("sched_kernel");
+  return GF_OK;
+}
+
 int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
   g->cta_threshold = thr > 0 ? thr : kDefaultCtaThreshold;
   GF_CHECK_CUDA(cudaGetDevice(&g->device));
@@ -115,8 +131,13 @@ int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
   int rc = build_schedule(g->row_ptr, g->n, g->cta_threshold, g->row_order, g->n_cta_rows,
                           g->n_empty_rows, g->n_small_rows, g->max_in, s);
   if (rc) return rc;
-  return build_schedule(g->csc_ptr, g->n, g->cta_threshold, g->col_order, g->n_cta_cols,
-                        g->n_empty_cols, g->n_small_cols, g->max_out, s);
+  rc = build_schedule(g->csc_ptr, g->n, g->cta_threshold, g->col_order, g->n_cta_cols,
+                      g->n_empty_cols, g->n_small_cols, g->max_out, s);
+  if (rc) return rc;
+  if ((rc = build_sched(g->row_order, g->row_ptr, g->n, &g->row_sched, s))) return rc;
+  if ((rc = build_sched(g->col_order, g->csc_ptr, g->n, &g->col_sched, s))) return rc;
+  GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
 }
 
 void free_graph(DevGraph* g) {
@@ -127,6 +148,8 @@ void free_graph(DevGraph* g) {
   cudaFree(g->csc_row);
   cudaFree(g->row_order);
   cudaFree(g->col_order);
+  cudaFree(g->row_sched);
+  cudaFree(g->col_sched);
   cudaFree(g->coo_dst);
   cudaFree(g->csc_perm);
   delete g;

@@ -57,6 +57,10 @@ struct DevGraph {
   int32_t* csc_row = nullptr;
   int32_t* row_order = nullptr;
   int32_t* col_order = nullptr;
+  // per schedule slot {node, first edge, end edge, 0}: one 16 B load replaces
+  // the dependent order -> pointer loads of a row's prologue
+  int4* row_sched = nullptr;
+  int4* col_sched = nullptr;
   int32_t cta_threshold = 0;
   int32_t n_cta_rows = 0, n_empty_rows = 0;
   int32_t n_cta_cols = 0, n_empty_cols = 0;
@@ -124,6 +128,7 @@ struct FwdArgs {
   int H, D, F, LPH;
   int l2;
   T scale, slope;
+  const int4* sched = nullptr;  // {node, begin, end} per slot (fast kernels)
   const T* Q;  // dot: N x F; add: el N x H
   const T* K;  // dot: N x F; add: er N x H
   const T* V;
@@ -143,6 +148,7 @@ struct BwdArgs {
   int H, D, F, LPH;
   int l2;
   T scale, slope;
+  const int4* sched = nullptr;
   const T* Q;
   const T* K;
   const T* V;

@@ -175,6 +175,7 @@ FwdArgs<T> base_args(const DevGraph& g, int H, int D, bool csc) {
   a.ptr = csc ? g.csc_ptr : g.row_ptr;
   a.idx = csc ? g.csc_row : g.col;
   a.order = csc ? g.col_order : g.row_order;
+  a.sched = csc ? g.col_sched : g.row_sched;
   a.n = csc ? g.active_cols() : g.active_rows();
   a.n_cta = csc ? g.n_cta_cols : g.n_cta_rows;
   a.H = H;
