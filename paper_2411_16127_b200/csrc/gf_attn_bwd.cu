@@ -83,7 +83,8 @@ __device__ __forceinline__ void warp_sum(T (&x)[NV]) {
 // ------------------------------------------------------------ pass A ------
 template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
 __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, const int warp,
-                                        const bool cta, const int slot, const bool live) {
+                                        const bool cta, const int slot, const bool live,
+                                        const int nrows) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -91,10 +92,17 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
-  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
+  // nrows consecutive warp rows, software-pipelined like fwd_row (gf_attn_fwd.cu)
+  const int4 zero4 = make_int4(0, 0, 0, 0);
+  int4 rs = live ? ld_sched(a.sched + slot) : zero4;
+  int4 rsn = nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
+  int nxt = 0;
+  for (int r = 0; r < nrows; ++r) {
+  const int4 rsnn = r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
   const int v = rs.x;
   int eb = rs.y, ee = rs.z;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
 
   const int h = c / a.LPH;
   const int off = h * a.D + (c % a.LPH) * NE;
@@ -136,12 +144,15 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
 
   constexpr int ep = pk ? 1 : EPW;
   const int js = pk ? 0 : sub;
-  int nxt = !pk && eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
   for (int base = eb; pk || base < ee; base += 32) {
     const int cnt = pk ? ee - eb : min(32, ee - base);
     const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
     const int myu = nxt;
-    if (!pk) nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
+    if (!pk) {
+      const int nb = base + 32;
+      nxt = nb < ee ? (nb + lane < ee ? ld_idx(a.idx + nb + lane) : 0)
+                    : (rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0);
+    }
 #pragma unroll 1
     for (int j0 = 0; j0 < cntw; j0 += ep * U) {
       bool ok[U];
@@ -200,6 +211,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
     }
     if (pk) break;
   }
+  if (!pk && eb >= ee) nxt = rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0;
 
   if (!pk) warp_sum<T, LPE, NA>(acc);
   if (cta && !cta_sum<T, LPE, NA>(acc, warp, c, sub)) return;
@@ -217,6 +229,9 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
     a.stats[4 * ri + 3] = delta;
     if constexpr (VAR == GF_ADD) a.dK[ri] = acc[0];
   }
+  rs = rsn;
+  rsn = rsnn;
+  }  // rows
 }
 
 // Bucket dispatch shared by both passes: CTA rows, warp rows, packed rows.
@@ -224,16 +239,18 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int EPW = 32 / LPE;                                                                 \
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;                                   \
   const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);                                 \
-  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {                         \
-    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp; \
-    if (!cta && slot >= a.pk0) return;                                                          \
-    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true);                         \
+  if (cta) {                                                                                    \
+    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, true, blockIdx.x, true, 1);               \
+  } else if (blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {                         \
+    const int slot = a.n_cta + ((blockIdx.x - a.n_cta) * kWarpsPerBlock + warp) * a.rpw;        \
+    if (slot >= a.pk0) return;                                                                  \
+    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, false, slot, true, min(a.rpw, a.pk0 - slot)); \
   } else if constexpr (EPW > 1) {                                                               \
     const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW + \
                      lane / LPE;                                                                \
     const bool live = slot < a.n;                                                               \
     if (!__any_sync(kFull, live)) return;                                                       \
-    ROWFN<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live);                        \
+    ROWFN<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1);                     \
   }
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
@@ -244,7 +261,8 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_r
 // ------------------------------------------------------------ pass B ------
 template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
 __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, const int warp,
-                                        const bool cta, const int slot, const bool live) {
+                                        const bool cta, const int slot, const bool live,
+                                        int /*nrows: pass B runs one column per warp, see below*/) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -252,9 +270,10 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
   constexpr bool pk = PK;  // packed column: this LPE-lane group owns the column
   const int c = lane % LPE, sub = lane / LPE;
-  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
-  const int u = rs.x;
-  int sb = rs.y, se = rs.z;
+  // No row pipelining / 16 B schedule entries here: at pass B's 64-register
+  // budget (4 CTAs/SM) either spills; the launcher keeps rpw = 1.
+  const int u = live ? __ldg(a.order + slot) : 0;
+  int sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
   if (cta) split_range(sb, se, kWarpsPerBlock, warp, sb, se);
 
   const int h = c / a.LPH;
@@ -378,7 +397,22 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
-  GF_BWD_DISPATCH(bwd_col)
+  // one call site for CTA and warp columns (runtime `cta`): two inlined copies
+  // push pass B past its 64-register budget
+  constexpr int EPW = 32 / LPE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
+  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
+    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
+    if (!cta && slot >= a.pk0) return;
+    bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1);
+  } else if constexpr (EPW > 1) {
+    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW +
+                     lane / LPE;
+    const bool live = slot < a.n;
+    if (!__any_sync(kFull, live)) return;
+    bwd_col<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1);
+  }
 }
 
 // ----------------------------------------------------------- generic path --
@@ -608,10 +642,13 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   ra.LPH = ca.LPH = fs.ok ? fs.lph : 1;
   // bucket geometry (see fwd): warp bucket [n_cta, pk0), packed [pk0, n)
   const int epw = fs.ok ? 32 / fs.lpe : 1;
+  // warp rows per warp: 8 for short rows (average degree <= 64), else 1 (as fwd)
+  ca.rpw = 1;  // pass B: no row pipelining (register budget, see bwd_col)
   auto buckets = [&](BwdArgs<T>& x, int n_small, int n_empty) {
     x.pk0 = epw > 1 ? std::max(x.n_cta, g.n - n_empty - n_small) : x.n;
     x.pk0 = std::min(x.pk0, x.n);
-    x.wblocks = (x.pk0 - x.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (&x == &ra) x.rpw = rows_per_warp(g.e, g.n, x.pk0 - x.n_cta);
+    x.wblocks = (x.pk0 - x.n_cta + kWarpsPerBlock * x.rpw - 1) / (kWarpsPerBlock * x.rpw);
     const int per_block = kWarpsPerBlock * epw;
     return x.n_cta + x.wblocks + (x.n - x.pk0 + per_block - 1) / per_block;
   };

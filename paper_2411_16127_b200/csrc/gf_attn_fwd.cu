@@ -40,20 +40,25 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
 // MODE 0: SMMF (scores computed here); 1: PMF's fused softmax + SpMM over the
 // scores an edge-parallel SDDMM wrote to a.ES; 2: the unfused SpMM (a.ES holds
 // normalised probabilities: O = sum p V, no softmax, no records).
-// One row (CTA slice, warp row, or — PK — one packed row per LPE-lane group).
+// Rows slot .. slot+nrows-1 (a CTA slice, nrows warp rows, or — PK — one
+// packed row per LPE-lane group).  Warp rows are software-pipelined: the
+// schedule entry two rows ahead and the next row's first 32 ids are loaded
+// while the current row's gathers are in flight, so consecutive rows do not
+// each pay the id round trip before their first gather.
 template <typename T, int CB, int LPE, int CPL, int VAR, int MODE, bool PK>
 __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, const int warp,
-                                        const bool cta, const int slot, const bool live) {
+                                        const bool cta, const int slot, const bool live,
+                                        const int nrows) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
   constexpr int U = CPL == 1 ? GF_U_FWD : GF_U2;
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
-  const int4 rs = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
-  const int v = rs.x;
-  int eb = rs.y, ee = rs.z;
-  if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  const int4 zero4 = make_int4(0, 0, 0, 0);
+  int4 rs = live ? ld_sched(a.sched + slot) : zero4;
+  int4 rsn = nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
+  int nxt = 0;
 
   const int h = c / a.LPH;
   const int off = h * a.D + (c % a.LPH) * NE;  // first element owned by this lane
@@ -61,6 +66,13 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
   const T* __restrict__ Sb = a.ES + h;        // MODE 1/2: ES[e * H + h]
+
+  for (int r = 0; r < nrows; ++r) {
+  const int4 rsnn = r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
+  const int v = rs.x;
+  int eb = rs.y, ee = rs.z;
+  if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
 
   // Destination-side operands stay in registers for the whole row.
   T kv[NE];
@@ -93,12 +105,15 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   // <= kSmallDegree edges one per step, loading ids directly.
   constexpr int ep = pk ? 1 : EPW;
   const int js = pk ? 0 : sub;
-  int nxt = !pk && eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
   for (int base = eb; pk || base < ee; base += 32) {
     const int cnt = pk ? ee - eb : min(32, ee - base);
     const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
-    const int myu = nxt;  // ids of this 32-edge chunk; prefetch the next one
-    if (!pk) nxt = base + 32 + lane < ee ? ld_idx(a.idx + base + 32 + lane) : 0;
+    const int myu = nxt;  // ids of this 32-edge chunk; prefetch the next one (or the next row's first)
+    if (!pk) {
+      const int nb = base + 32;
+      nxt = nb < ee ? (nb + lane < ee ? ld_idx(a.idx + nb + lane) : 0)
+                    : (rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0);
+    }
 #pragma unroll 1
     for (int j0 = 0; j0 < cntw; j0 += ep * U) {
       bool ok[U];
@@ -172,6 +187,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
     }
     if (pk) break;
   }
+  if (!pk && eb >= ee) nxt = rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0;
 
   // Merge the EPW edge slots of the warp (butterfly: every lane ends with
   // the warp's state); packed groups each own a row and skip it.
@@ -239,6 +255,9 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       rec[2] = VAR == GF_DOT ? rk : erv;
     }
   }
+  rs = rsn;
+  rsn = rsnn;
+  }  // rows
 }
 
 // Three buckets (degree-descending order): CTA rows (edge-split over 8
@@ -249,16 +268,19 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fa
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
-    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
-    if (!cta && slot >= a.pk0) return;
-    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, cta, slot, true);
+  if (cta) {
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, true, blockIdx.x, true, 1);
+  } else if (blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
+    const int slot = a.n_cta + ((blockIdx.x - a.n_cta) * kWarpsPerBlock + warp) * a.rpw;
+    if (slot >= a.pk0) return;
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, false, slot, true,
+                                               min(a.rpw, a.pk0 - slot));
   } else if constexpr (EPW > 1) {
     const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW +
                      lane / LPE;
     const bool live = slot < a.n;
     if (!__any_sync(kFull, live)) return;
-    fwd_row<T, CB, LPE, CPL, VAR, MODE, true>(a, lane, warp, false, slot, live);
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, true>(a, lane, warp, false, slot, live, 1);
   }
 }
 
@@ -429,7 +451,11 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     // a warp holds more than one edge slot
     a.pk0 = epw > 1 ? std::max(a.n_cta, g.n - g.n_empty_rows - g.n_small_rows) : a.n;
     a.pk0 = std::min(a.pk0, a.n);
-    a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    // Short rows (average degree <= 64, e.g. ogbn-products ~26) are latency-
+    // bound on their prologue: give each warp 8 consecutive rows and pipeline
+    // them; long rows (Reddit ~490) keep one row per warp (A/B, profiles/).
+    a.rpw = rows_per_warp(g.e, g.n, a.pk0 - a.n_cta);
+    a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock * a.rpw - 1) / (kWarpsPerBlock * a.rpw);
     const int rows_per_block = kWarpsPerBlock * epw;
     const int blocks = a.n_cta + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;
     const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -114,6 +115,15 @@ struct DevGraph {
 
 constexpr int kDefaultCtaThreshold = 1024;
 constexpr int kSmallDegree = 8;  // packed (sub-warp) bucket: degree 1..8
+
+// Warp-bucket rows per warp: software-pipelined row prologues pay off for
+// short rows (average degree <= 64) but only while every SM still gets ~4
+// waves of resident warps (148 SMs x 24 warps); otherwise one row per warp.
+inline int rows_per_warp(int64_t edges, int64_t nodes, int64_t warp_rows) {
+  if (edges > 64 * std::max<int64_t>(1, nodes)) return 1;
+  const int64_t r = warp_rows / (148 * 24 * 4);
+  return r >= 8 ? 8 : r >= 4 ? 4 : r >= 2 ? 2 : 1;
+}
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
 
 // ---------------------------------------------------------- kernel params --
@@ -135,6 +145,7 @@ struct FwdArgs {
   T* O;
   T* stats;  // N x H x 4 records (gf_device.cuh Rec)
   int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
+  int rpw = 1;               // warp-bucket rows per warp (software-pipelined prologues)
   const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
   const int32_t* eperm = nullptr;  // MODE 3: slot -> CSR edge id of ES (CSC passes)
 };
@@ -159,6 +170,7 @@ struct BwdArgs {
   T* dK;     // pass A (dot) / der (add)
   T* dV;     // pass B
   int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
+  int rpw = 1;               // warp-bucket rows per warp
 };
 
 // Launchers (defined in gf_attn_fwd.cu / gf_attn_bwd.cu).
