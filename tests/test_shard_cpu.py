@@ -3,7 +3,8 @@
 Each rank builds its shard of the same graph and checks that (1) the shards
 partition the edge set exactly on both the CSR and the CSC side, (2) each
 row / column keeps its edge order (monotonic relabelling), (3) the in-place
-all-gather of padded node tables reproduces the full table, and (4) the
+all-gather of padded node tables reproduces the full table (also with several
+asynchronous all-gathers in flight, as the bench step issues them), and (4) the
 forward restricted to the rank's rows (CPU oracle on the shard CSR) equals
 the single-process forward bitwise on the owned rows.
 """
@@ -81,6 +82,18 @@ def worker(rank, world, port, errq):
         mine[sh.block] = full[sh.block]
         all_gather_rows(mine, sh)
         assert torch.equal(mine, full)
+        # (3b) the bench step's overlapped order: several async all-gathers in
+        # flight, waited on in need order (V, Q first; dO, K later)
+        tabs = [sh.to_padded(t(x)) for x in (V, Q, K, Q * 2)]
+        mines = []
+        for x in tabs:
+            m = torch.zeros_like(x)
+            m[sh.block] = x[sh.block]
+            mines.append(m)
+        works = [all_gather_rows(m, sh, async_op=True) for m in mines]
+        for w in works:
+            w.wait()
+        assert all(torch.equal(m, x) for m, x in zip(mines, tabs))
         # (4) sharded forward == single-process forward on owned rows, bitwise
         csr = oracle.CSR(sh.n_padded, rp, col, cp, cr, np.zeros(len(cr), np.int64))
         Op = oracle.forward(csr, sh.to_padded(t(Q)).numpy(), sh.to_padded(t(K)).numpy(),
