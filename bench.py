@@ -60,35 +60,28 @@ def reddit_degrees(np):
 
 
 def gen_graph_device(name, device, seed=0):
-    """Synthetic graph on the GPU: returns (n, src, dst) int64 device tensors,
-    unique edges (setup only; the canonical CSR/CSC is then built by the
-    device from_coo kernel, bit-exact with the reference's from_coo)."""
+    """Synthetic graph generated on the GPU by this package's device
+    generators (gf_gen_*_device: counter-hashed draws + radix-sort dedup;
+    setup only): returns (n, src, dst) int64 device tensors of distinct edges.
+    The canonical CSR/CSC is then built by the device from_coo kernel,
+    bit-exact with the reference's from_coo."""
     import numpy as np
     import torch
 
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
+    from paper_2411_16127_b200 import fused
+
     if name == "reddit":
-        # Chung-Lu-style in-degree sequence deg_i = round(21657 (i+1)^-0.34),
-        # node ids randomly permuted, uniform sources; duplicates dropped.
-        n = REDDIT_N
-        deg = torch.from_numpy(reddit_degrees(np)).to(device)
-        perm = torch.randperm(n, device=device, generator=g)
-        dst = torch.repeat_interleave(perm, deg)
-        src = torch.randint(0, n, (dst.numel(),), device=device, generator=g)
-    elif name == "products":
-        n, e = 2_400_000, 62_000_000
-        src = torch.randint(0, n, (e,), device=device, generator=g)
-        dst = torch.randint(0, n, (e,), device=device, generator=g)
-    elif name == "pubmed":
-        n, e = 19_717, 88_648
-        src = torch.randint(0, n, (e,), device=device, generator=g)
-        dst = torch.randint(0, n, (e,), device=device, generator=g)
-    elif name == "cora":
-        n, e = 2_708, 10_556
-        src = torch.randint(0, n, (e,), device=device, generator=g)
-        dst = torch.randint(0, n, (e,), device=device, generator=g)
-    elif name == "molhiv":
+        # Chung-Lu-style in-degree sequence deg_i = round(21657 (i+1)^-0.34) on
+        # hashed node ids, uniform sources, duplicate sources dropped
+        src, dst = fused.gen_power_law_device(REDDIT_N, REDDIT_MAX, REDDIT_EXP, seed=seed,
+                                              device=device)
+        return REDDIT_N, src, dst
+    if name in ("products", "pubmed", "cora"):
+        n, e = {"products": (2_400_000, 62_000_000), "pubmed": (19_717, 88_648),
+                "cora": (2_708, 10_556)}[name]
+        src, dst = fused.gen_random_device(n, e / n, seed=seed, device=device)
+        return n, src, dst
+    if name == "molhiv":
         # 1024 molecules of 26 atoms: a random spanning tree + 3 ring bonds,
         # bonds in both directions (~25.5 atoms / 27.5 bonds per ogbg-molhiv graph).
         mols, atoms = 1024, 26
@@ -106,10 +99,9 @@ def gen_graph_device(name, device, seed=0):
         dst = torch.tensor(d_all, device=device)
         keep = src != dst
         src, dst = src[keep], dst[keep]
-    else:
-        raise ValueError(name)
-    key = torch.unique(dst.to(torch.int64) * n + src.to(torch.int64))
-    return n, key % n, key // n
+        key = torch.unique(dst.to(torch.int64) * n + src.to(torch.int64))
+        return n, key % n, key // n
+    raise ValueError(name)
 
 
 # ----------------------------------------------------------- measurement --

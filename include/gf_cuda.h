@@ -236,6 +236,27 @@ int gf_gat_fanin(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf,
                  const void* a_r, const void* dV, const void* del, const void* der, void* dH,
                  void* da_l, void* da_r, void* stream);
 
+/* ---- synthetic graphs on the device ----
+ * The reference's generators' distributions (graph.cpp:127-185), drawn with
+ * counter-based hashing + radix-sort dedup instead of a sequential
+ * mt19937_64 rejection loop: deterministic per seed, NOT the reference's
+ * exact edge sequence.  Output: device int64 COO (src, dst) for
+ * gf_from_coo_device; *e_out = edges written.
+ *   random     : exactly round(n*avg_degree) distinct uniform edges
+ *   super_node : node 0 gets exactly hub_degree distinct in-neighbours, the
+ *                rest (max(hub, round(n*avg)) edges in total) uniform distinct
+ *                edges with destinations != 0
+ *   power_law  : row r of deg_r = round(max_degree (r+1)^-exponent) is a
+ *                hashed node id, sources uniform, duplicate sources dropped
+ *                (capacity >= sum deg_r) */
+int gf_gen_random_device(int64_t n, double avg_degree, uint64_t seed, int64_t* src, int64_t* dst,
+                         int64_t* e_out, void* stream);
+int gf_gen_super_node_device(int64_t n, double avg_degree, int64_t hub_degree, uint64_t seed,
+                             int64_t* src, int64_t* dst, int64_t* e_out, void* stream);
+int gf_gen_power_law_device(int64_t n, int64_t max_degree, double exponent, uint64_t seed,
+                            int64_t capacity, int64_t* src, int64_t* dst, int64_t* e_out,
+                            void* stream);
+
 /* ---- diagnostics ----
  * Measured gather bandwidth (GB/s) of rows of row_bytes (32..1024, lanes read
  * consecutive 32 B chunks with 256-bit non-coherent loads) chosen in hashed

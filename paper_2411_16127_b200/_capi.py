@@ -75,6 +75,12 @@ SIGNATURES = {
                                    _vp]),
     "gf_softmax_backward": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
     "gf_sddmm_backward": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gf_gen_random_device": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _vp, _vp,
+                                       C.POINTER(C.c_int64), _vp]),
+    "gf_gen_super_node_device": (C.c_int, [C.c_int64, C.c_double, C.c_int64, C.c_uint64, _vp, _vp,
+                                           C.POINTER(C.c_int64), _vp]),
+    "gf_gen_power_law_device": (C.c_int, [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_int64,
+                                          _vp, _vp, C.POINTER(C.c_int64), _vp]),
     "gf_measure_l2_gather": (C.c_int, [C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

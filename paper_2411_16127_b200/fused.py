@@ -337,3 +337,39 @@ def attn_backward_unfused(g: DeviceGraph, spec: AttnSpec, Q, K, V, P, dO, stream
     dS = softmax_backward(g, spec.heads, P, dP, stream=stream)
     dQ, dK = sddmm_backward(g, spec, Q, K, dS, stream=stream)
     return dQ, dK, dV, dP, dS
+
+
+# ---- synthetic graphs on the device (gf_cuda.h "synthetic graphs") ---------
+def gen_random_device(n, avg_degree, seed=0, device="cuda", stream=None):
+    """(src, dst) int64 device COO: exactly round(n*avg) distinct uniform edges."""
+    e = int(avg_degree * n + 0.5)
+    src = torch.empty(max(e, 1), dtype=torch.int64, device=device)
+    dst = torch.empty_like(src)
+    out = C.c_int64()
+    check(lib().gf_gen_random_device(n, float(avg_degree), seed, _p(src), _p(dst), C.byref(out),
+                                     _stream(stream)), "gf_gen_random_device")
+    return src[: out.value], dst[: out.value]
+
+
+def gen_super_node_device(n, avg_degree, hub_degree, seed=0, device="cuda", stream=None):
+    """(src, dst): node 0 with exactly hub_degree in-neighbours + uniform edges."""
+    e = max(hub_degree, int(avg_degree * n + 0.5))
+    src = torch.empty(max(e, 1), dtype=torch.int64, device=device)
+    dst = torch.empty_like(src)
+    out = C.c_int64()
+    check(lib().gf_gen_super_node_device(n, float(avg_degree), hub_degree, seed, _p(src), _p(dst),
+                                         C.byref(out), _stream(stream)),
+          "gf_gen_super_node_device")
+    return src[: out.value], dst[: out.value]
+
+
+def gen_power_law_device(n, max_degree, exponent, seed=0, device="cuda", stream=None):
+    """(src, dst): in-degree sequence round(max (r+1)^-exponent) on hashed ids."""
+    cap = int(np.rint(max_degree * (np.arange(n, dtype=np.float64) + 1.0) ** -exponent).sum())
+    src = torch.empty(max(cap, 1), dtype=torch.int64, device=device)
+    dst = torch.empty_like(src)
+    out = C.c_int64()
+    check(lib().gf_gen_power_law_device(n, max_degree, float(exponent), seed, cap, _p(src),
+                                        _p(dst), C.byref(out), _stream(stream)),
+          "gf_gen_power_law_device")
+    return src[: out.value], dst[: out.value]

@@ -1,0 +1,64 @@
+"""GPU: the device synthetic-graph generators.  They
+follow the reference generators' distributions (graph.cpp:127-185) with
+counter-based hashing instead of a sequential mt19937_64 rejection loop, so
+the contract checked here is distributional: exact edge counts, distinct
+edges, ids in range, the hub's exact in-degree, the power-law degree
+sequence, determinism per seed, and that the result feeds the device
+from_coo (no duplicate is rejected)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _keys(src, dst, n):
+    return (dst.cpu().numpy().astype(np.int64) * n + src.cpu().numpy())
+
+
+@pytest.mark.parametrize("n,avg", [(1000, 3.5), (2708, 3.898), (300, 150.0), (50_000, 25.8)])
+def test_gen_random_device(cuda, n, avg):
+    from paper_2411_16127_b200 import fused
+
+    src, dst = fused.gen_random_device(n, avg, seed=7)
+    k = _keys(src, dst, n)
+    assert len(k) == int(avg * n + 0.5)
+    assert len(np.unique(k)) == len(k)
+    assert src.min() >= 0 and src.max() < n and dst.min() >= 0 and dst.max() < n
+    s2, d2 = fused.gen_random_device(n, avg, seed=7)
+    assert torch.equal(src, s2) and torch.equal(dst, d2)  # deterministic per seed
+    s3, _ = fused.gen_random_device(n, avg, seed=8)
+    assert not torch.equal(src, s3)
+    # uniform: every destination decile gets ~10% of the edges
+    hist = np.bincount(dst.cpu().numpy() * 10 // n, minlength=10) / len(k)
+    assert np.all(np.abs(hist - 0.1) < 0.03), hist
+    # feeds the device from_coo without a duplicate rejection
+    row_ptr, col, _, _, _ = fused.from_coo_device(n, src, dst)
+    assert int(row_ptr[-1]) == len(k)
+
+
+def test_gen_super_node_device(cuda):
+    from paper_2411_16127_b200 import fused
+
+    n, avg, hub = 3000, 3.0, 2500
+    src, dst = fused.gen_super_node_device(n, avg, hub, seed=1)
+    k = _keys(src, dst, n)
+    assert len(k) == max(hub, int(avg * n + 0.5)) and len(np.unique(k)) == len(k)
+    deg = np.bincount(dst.cpu().numpy(), minlength=n)
+    assert deg[0] == hub  # exact hub in-degree
+    assert deg[1:].max() < hub  # every other in-degree strictly below it
+    assert len(np.unique(src.cpu().numpy()[dst.cpu().numpy() == 0])) == hub
+
+
+def test_gen_power_law_device(cuda):
+    from paper_2411_16127_b200 import fused
+
+    n, mx, ex = 20_000, 2_000, 0.34
+    src, dst = fused.gen_power_law_device(n, mx, ex, seed=3)
+    k = _keys(src, dst, n)
+    assert len(np.unique(k)) == len(k)
+    want = np.sort(np.rint(mx * (np.arange(n) + 1.0) ** -ex).astype(np.int64))[::-1]
+    got = np.sort(np.bincount(dst.cpu().numpy(), minlength=n))[::-1]
+    # duplicate sources are dropped: each row loses at most a few edges
+    assert np.all(got <= want) and np.all(want - got <= np.maximum(3, want * want // n + 3))
+    assert got[0] >= mx - mx * mx // n - 5  # ~mx^2/(2n) birthday collisions
