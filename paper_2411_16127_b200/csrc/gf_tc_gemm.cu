@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // were tried first and produced all-zero accumulators on B200.)
 // Deterministic split-K: CTA z owns K rows [z*Ks, (z+1)*Ks) and writes its
 // M x N partial; a fixed-order reduction sums the partials.
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, 3)
     tc_gemm_tn_3xtf32(int M, int N, int K, int ks, const float* __restrict__ A,
                       const float* __restrict__ B, float* __restrict__ part) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -259,19 +259,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = instr_desc_tf32(TC_M, NP);  // both operands K-major
   const uint32_t lbo_a = 16 * 128, lbo_b = (NP / 8) * 128, sbo = 128;
+  // The launcher caps the K slice at kTnMaxSlice rows: the tensor core's
+  // truncating accumulation then spans <= 1024 products per element, and the
+  // fp32 partials are summed round-to-nearest in a fixed order (tn_reduce*).
   const int kb = blockIdx.x * ks, ke = min(K, kb + ks);
   uint32_t phase = 0;
-  // fp32 round-to-nearest accumulator in smem (row stride NP + 4: conflict-free
-  // float4 rows); TMEM accumulates at most kSub K rows before it is drained
-  // here, bounding the tensor core's truncating accumulation error.
-  constexpr int kSub = 1024;
-  float* acc_s = b_lo + NP * TC_KC;
-  const int AS = NP + 4;
-  for (int i = t; i < TC_M * AS; i += TC_THREADS) acc_s[i] = 0.f;
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-  int sub0 = kb;
   for (int k0 = kb; k0 < ke; k0 += TC_KC) {
-    if (k0 - sub0 >= kSub) sub0 = k0;
     // A^T chunk: thread t = output row m, 4 K rows per float4 (K-major cores)
 #pragma unroll
     for (int kc = 0; kc < TC_KC / 4; ++kc) {
@@ -321,7 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t da = s * 2 * lbo_a, db = s * 2 * lbo_b;
         const uint64_t dah = smem_desc(ah + da, lbo_a, sbo), dal = smem_desc(al + da, lbo_a, sbo);
         const uint64_t dbh = smem_desc(bh + db, lbo_b, sbo), dbl = smem_desc(bl + db, lbo_b, sbo);
-        mma_tf32(tmem, dah, dbh, idesc, (k0 > sub0 || s > 0) ? 1u : 0u);
+        mma_tf32(tmem, dah, dbh, idesc, (k0 > kb || s > 0) ? 1u : 0u);
         mma_tf32(tmem, dah, dbl, idesc, 1u);
         mma_tf32(tmem, dal, dbh, idesc, 1u);
       }
@@ -330,27 +324,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     mbar_wait(smem_u32(&mbar), phase);
     phase ^= 1;
-    const int nk = k0 + TC_KC;
-    if (nk >= ke || nk - sub0 >= kSub) {  // drain this sub-slice: TMEM -> smem (RN adds)
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int c = 0; c < NP; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + lane_base + c, r);
-        float* a = acc_s + t * AS + c;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] += __uint_as_float(r[j]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncthreads();  // TMEM reads complete before the next sub-slice's MMAs
-    }
   }
+  // epilogue: TMEM -> this split's partial (thread = output row m)
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int row = t;
   float* dst = part + static_cast<size_t>(blockIdx.x) * M * N + static_cast<size_t>(row) * N;
   for (int c = 0; c < NP; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + lane_base + c, r);
     if (row < M) {
 #pragma unroll
       for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(dst + c + j) = *reinterpret_cast<const float4*>(acc_s + t * AS + c + j);
+        *reinterpret_cast<float4*>(dst + c + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -369,6 +356,20 @@ __global__ void tn_reduce(const float* __restrict__ part, int splits, size_t mn,
   }
 }
 
+// First level of the fixed-order reduction for many splits: block (x, g)
+// sums splits [g*per, (g+1)*per) of its elements into part2[g].
+__global__ void tn_reduce_group(const float* __restrict__ part, int splits, int per, size_t mn,
+                                float* __restrict__ part2) {
+  const int g = blockIdx.y;
+  const int z0 = g * per, z1 = min(splits, z0 + per);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < mn;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int z = z0; z < z1; ++z) s += part[z * mn + i];
+    part2[g * mn + i] = s;
+  }
+}
+
 }  // namespace
 
 bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
@@ -381,14 +382,17 @@ bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void*
 
 int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
                int accumulate, cudaStream_t s) {
-  const int64_t target = std::min<int64_t>(296, (K + 1023) / 1024);
-  int64_t ks = (K + target - 1) / target;
-  ks = ((ks + TC_KC - 1) / TC_KC) * TC_KC;
+  // K slices: enough CTAs for ~4 per SM, each <= kTnMaxSlice rows (a multiple
+  // of the 32-row chunk); every CTA writes one fp32 partial
+  constexpr int64_t kTnMaxSlice = 1024;
+  int64_t ks = (K + 148 * 4 - 1) / (148 * 4);
+  ks = std::min<int64_t>(kTnMaxSlice, std::max<int64_t>(TC_KC, (ks + TC_KC - 1) / TC_KC * TC_KC));
   const int splits = static_cast<int>((K + ks - 1) / ks);
+  constexpr int kPer = 64;  // splits summed per first-level group
+  const int groups = splits > kPer ? (splits + kPer - 1) / kPer : 0;
   float* part = nullptr;
-  GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(float) * splits * M * N, s));
-  const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC +
-                                      TC_M * static_cast<size_t>(N + 4));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(float) * (splits + groups) * M * N, s));
+  const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(N) * TC_KC);
   GF_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_tn_3xtf32,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
@@ -397,8 +401,15 @@ int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, 
                                                      B, part);
   GF_CHECK_LAUNCH("tc_gemm_tn_3xtf32");
   const size_t mn = static_cast<size_t>(M) * N;
-  tn_reduce<<<static_cast<int>(std::min<size_t>(1024, (mn + 255) / 256)), 256, 0, s>>>(
-      part, splits, mn, C, accumulate);
+  const int rblocks = static_cast<int>(std::min<size_t>(1024, (mn + 255) / 256));
+  if (groups) {  // two fixed-order levels: groups of kPer splits, then the groups
+    float* part2 = part + static_cast<size_t>(splits) * mn;
+    tn_reduce_group<<<dim3(rblocks, groups), 256, 0, s>>>(part, splits, kPer, mn, part2);
+    GF_CHECK_LAUNCH("tn_reduce_group");
+    tn_reduce<<<rblocks, 256, 0, s>>>(part2, groups, mn, C, accumulate);
+  } else {
+    tn_reduce<<<rblocks, 256, 0, s>>>(part, splits, mn, C, accumulate);
+  }
   GF_CHECK_LAUNCH("tn_reduce");
   cudaFreeAsync(part, s);
   return GF_OK;
