@@ -87,7 +87,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 
-// C[M x N] = A[M x K] * B[K x N], all row-major fp32.  grid = (ceil(M/128), N/n_tile).
+// C[M x N] = A[M x K] * B[K x N], all row-major fp32.  1-D grid over
+// (m tile, n tile) with the n tile fastest, so the CTAs that share an A tile
+// run together and all but the first read it from L2.  The next 32-K chunk
+// of A and B is loaded into registers while the tensor core works on the
+// current one (software pipelining across the smem stage).
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_3xtf32(int M, int N, int K, int n_tile, const float* __restrict__ A,
                    const float* __restrict__ B, float* __restrict__ C, int accumulate) {
@@ -95,7 +99,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int m0 = blockIdx.x * TC_M, n0 = blockIdx.y * n_tile;
+  const int n_tiles = N / n_tile;
+  const int m0 = (blockIdx.x / n_tiles) * TC_M, n0 = (blockIdx.x % n_tiles) * n_tile;
   const int NT = n_tile;
   // smem: A_hi, A_lo (128 x 32 tf32 each, 16 KB), B_hi, B_lo (NT x 32, NT*128 B each)
   float* a_hi = reinterpret_cast<float*>(smem);
@@ -123,10 +128,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // B core (ng, kc) at (kc*NT/8 + ng)*128.  One MMA k-step = 2 kc.
   const uint32_t lbo_a = 16 * 128, lbo_b = (NT / 8) * 128, sbo = 128;
 
-  uint32_t phase = 0;
   const int row = m0 + t;
-  for (int k0 = 0; k0 < K; k0 += TC_KC) {
-    // ---- A chunk: thread t converts row m0+t, columns [k0, k0+32)
+  // register stage: thread t holds row m0+t of the A chunk and columns
+  // n0+t, n0+t+128 of the B chunk
+  float4 av[TC_KC / 4];
+  float bv[2][TC_KC];
+  auto load_chunk = [&](int k0) {
 #pragma unroll
     for (int kc = 0; kc < TC_KC / 4; ++kc) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -141,6 +148,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           v.z = k + 2 < K ? src[2] : 0.f;
         }
       }
+      av[kc] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int n = t + i * TC_THREADS;
+#pragma unroll
+      for (int j = 0; j < TC_KC; ++j) {
+        const int k = k0 + j;
+        bv[i][j] = (n < NT && k < K) ? __ldg(B + static_cast<size_t>(k) * N + n0 + n) : 0.f;
+      }
+    }
+  };
+
+  uint32_t phase = 0;
+  load_chunk(0);
+  for (int k0 = 0; k0 < K; k0 += TC_KC) {
+    // ---- A chunk (row m0+t) and B chunk (columns t, t+128) -> hi/lo tf32 in smem
+#pragma unroll
+    for (int kc = 0; kc < TC_KC / 4; ++kc) {
+      const float4 v = av[kc];
       float4 h, l;
       split_tf32(v.x, h.x, l.x);
       split_tf32(v.y, h.y, l.y);
@@ -150,21 +177,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       *reinterpret_cast<float4*>(a_hi + off) = h;
       *reinterpret_cast<float4*>(a_lo + off) = l;
     }
-    // ---- B chunk: B[k][n0+n] for n in [0, NT): thread handles n = t, t+128
-    for (int n = t; n < NT; n += TC_THREADS) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int n = t + i * TC_THREADS;
+      if (n >= NT) continue;
 #pragma unroll
       for (int kc = 0; kc < TC_KC / 4; ++kc) {
-        float w[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + kc * 4 + j;
-          w[j] = (k < K) ? B[static_cast<size_t>(k) * N + n0 + n] : 0.f;
-        }
         float4 h, l;
-        split_tf32(w[0], h.x, l.x);
-        split_tf32(w[1], h.y, l.y);
-        split_tf32(w[2], h.z, l.z);
-        split_tf32(w[3], h.w, l.w);
+        split_tf32(bv[i][kc * 4 + 0], h.x, l.x);
+        split_tf32(bv[i][kc * 4 + 1], h.y, l.y);
+        split_tf32(bv[i][kc * 4 + 2], h.z, l.z);
+        split_tf32(bv[i][kc * 4 + 3], h.w, l.w);
         const int off = (kc * (NT / 8) + n / 8) * 32 + (n % 8) * 4;
         *reinterpret_cast<float4*>(b_hi + off) = h;
         *reinterpret_cast<float4*>(b_lo + off) = l;
@@ -189,6 +212,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(&mbar)) : "memory");
     }
+    if (k0 + TC_KC < K) load_chunk(k0 + TC_KC);  // in flight under the MMAs
     mbar_wait(smem_u32(&mbar), phase);  // MMAs done: smem reusable, accumulator final
     phase ^= 1;
   }
@@ -437,8 +461,8 @@ int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, flo
   const size_t smem = sizeof(float) * (2 * TC_M * TC_KC + 2 * static_cast<size_t>(nt) * TC_KC);
   GF_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-  dim3 grid(static_cast<unsigned>((M + TC_M - 1) / TC_M), static_cast<unsigned>(N / nt));
-  tc_gemm_3xtf32<<<grid, TC_THREADS, smem, s>>>(static_cast<int>(M), static_cast<int>(N),
+  const int64_t grid = (M + TC_M - 1) / TC_M * (N / nt);
+  tc_gemm_3xtf32<<<static_cast<unsigned>(grid), TC_THREADS, smem, s>>>(static_cast<int>(M), static_cast<int>(N),
                                                 static_cast<int>(K), nt, A, B, C, accumulate);
   GF_CHECK_LAUNCH("tc_gemm_3xtf32");
   return GF_OK;
