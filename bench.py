@@ -386,8 +386,13 @@ def run_reference(args, rank, world):
     return 0
 
 
-def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush):
-    """Whole layer (projection + pipeline + weight grads) per step, fp32."""
+def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, shard=None):
+    """One full-graph training step of the layer, fp32 (models.hpp:104-158 +
+    an SGD update): projection of the owned rows (tcgen05 3xTF32), GAT
+    logits, [sharded: all-gather of the projected source rows], fused
+    attention forward + recompute backward, GAT fan-in, weight gradients
+    X^T dY over the owned rows (tcgen05), [sharded: all-reduce of dW], SGD
+    update of every weight.  X has width F (bench.cpp:86-87)."""
     import torch
 
     from paper_2411_16127_b200 import fused
@@ -399,59 +404,96 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush):
     dO = torch.rand(n, F, device=dev, generator=g) * 2 - 1
     rnd = lambda *s: (torch.rand(*s, device=dev, generator=g) * 2 - 1) * lim  # noqa: E731
     gat = layer == "gat"
+    lr = 1e-3
     Wv = rnd(F, F)
     if gat:
         al, ar = rnd(F), rnd(F)
     else:
         Wq, Wk = rnd(F, F), rnd(F, F)
-    Hf = torch.empty(n, F, device=dev)
-    Qb = torch.empty(n, F, device=dev)
-    Kb = torch.empty(n, F, device=dev)
+    rows = shard.block if shard is not None else slice(0, n)
+    Hf = torch.zeros(n, F, device=dev)
+    Qb = torch.zeros(n, F, device=dev)
+    Kb = torch.zeros(n, F, device=dev)
+    EL = torch.zeros(n, H, device=dev)
+    ER = torch.zeros(n, H, device=dev)
     O = torch.empty(n, F, device=dev)
-    st = torch.empty(n, H, 4, device=dev)
+    st = torch.zeros(n, H, 4, device=dev)
     qk = spec.qk_width
-    dQ, dK, dV = (torch.empty(n, qk, device=dev), torch.empty(n, qk, device=dev),
-                  torch.empty(n, F, device=dev))
+    dQ, dK, dV = (torch.zeros(n, qk, device=dev), torch.zeros(n, qk, device=dev),
+                  torch.zeros(n, F, device=dev))
     dW = [torch.empty(F, F, device=dev) for _ in range(3)]
+    Xr = X[rows]
+    if shard is not None:
+        import torch.distributed as dist
+
+        from paper_2411_16127_b200.shard import all_gather_rows
 
     def step(ev=None):
         rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
         rec(0)
         if gat:
-            fused.gemm(X, Wv, out=Hf, stream=stream)
-            el, er = fused.gat_logits(Hf, al, ar, H, D, stream=stream)
-            q, k, v = el, er, Hf
+            fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
+            fused.gat_logits(Hf[rows], al, ar, H, D, stream=stream, el=EL[rows], er=ER[rows])
+            q, k, v = EL, ER, Hf
         else:
-            fused.gemm(X, Wq, out=Qb, stream=stream)
-            fused.gemm(X, Wk, out=Kb, stream=stream)
-            fused.gemm(X, Wv, out=Hf, stream=stream)
+            fused.gemm(Xr, Wq, out=Qb[rows], stream=stream)
+            fused.gemm(Xr, Wk, out=Kb[rows], stream=stream)
+            fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
             q, k, v = Qb, Kb, Hf
+        later = []
+        if shard is not None:  # source rows first; dO (and K) under the forward / pass A
+            for w in [all_gather_rows(t, shard, async_op=True) for t in (v, q)]:
+                w.wait()
+            later = [all_gather_rows(t, shard, async_op=True)
+                     for t in (dO,) + (() if gat else (k,))]
         rec(1)
         fused.attn_forward(dg, spec, q, k, v, O=O, stats=st, stream=stream)
         fused.attn_backward_rows(dg, spec, q, k, v, O, st, dO, dK, stream=stream)
+        if shard is not None:
+            for w in later:
+                w.wait()
+            all_gather_rows(st, shard)
         fused.attn_backward_cols(dg, spec, q, k, v, st, dO, dQ, dV, stream=stream)
         rec(2)
         if gat:
-            dH, dal, dar = fused.gat_fanin(Hf, al, ar, dV, dQ, dK, H, D, stream=stream)
-            fused.gemm(X, dH, trans_a=True, out=dW[0], stream=stream)
+            dH, dal, dar = fused.gat_fanin(Hf[rows], al, ar, dV[rows], dQ[rows], dK[rows], H, D,
+                                           stream=stream)
+            fused.gemm(Xr, dH, trans_a=True, out=dW[0], stream=stream)
+            grads = [(Wv, dW[0]), (al, dal), (ar, dar)]
         else:
             for w_, d_ in zip(dW, (dQ, dK, dV)):
-                fused.gemm(X, d_, trans_a=True, out=w_, stream=stream)
+                fused.gemm(Xr, d_[rows], trans_a=True, out=w_, stream=stream)
+            grads = [(Wq, dW[0]), (Wk, dW[1]), (Wv, dW[2])]
+        if shard is not None:  # weight gradients are partial sums over the owned rows
+            for _, d_ in grads:
+                dist.all_reduce(d_)
         rec(3)
+        for w_, d_ in grads:  # SGD
+            w_.add_(d_, alpha=-lr)
+        rec(4)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     K = max(5, args.steps // 5)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    if shard is not None:
+        dist.barrier()
     for i in range(K):
         flush.zero_()
         step(evs[i])
     torch.cuda.synchronize()
     seg = lambda j: sum(a[j].elapsed_time(a[j + 1]) for a in evs) / K  # noqa: E731
-    ms = sum(a[0].elapsed_time(a[3]) for a in evs) / K
+    ms = sum(a[0].elapsed_time(a[4]) for a in evs) / K
+    if shard is not None:  # whole job: max over ranks
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     return {"value": e / (ms / 1e3) / 1e9, "unit": "GEdges/s", "ms_per_step": ms,
             "projection_fwd_ms": seg(0), "pipeline_ms": seg(1), "weight_grad_ms": seg(2),
+            "sgd_ms": seg(3),
+            "step": "projection (+ all-gather when sharded) -> fused attention fwd + recompute "
+                    "bwd -> GAT fan-in -> X^T dY (+ all-reduce when sharded) -> SGD update",
             "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; X^T*dY deterministic split-K)",
             "x_width": F}
 
@@ -786,8 +828,9 @@ def run_ours(args, rank, world):
     # F (bench.cpp:86-87): X·W on tcgen05 (3xTF32), GAT logits / fan-in,
     # the fused pipeline, and the weight gradients X^T·dH.
     layer_out = None
-    if not sharded and not args.no_layer:
-        layer_out = layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush)
+    if not args.no_layer:
+        layer_out = layer_step_timing(args, layer, spec, dg, n_tab, e, F, H, D, dev, stream, flush,
+                                      shard=shard)
     ablation = bwd_ablation = None
     if not sharded and not args.no_ablation:
         ablation = strategy_ablation(dg, spec, Q, K, V, O, stats, stream, flush)

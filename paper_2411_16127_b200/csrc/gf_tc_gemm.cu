@@ -289,40 +289,51 @@ __global__ void __launch_bounds__(TC_THREADS, 3)
   const int kb = blockIdx.x * ks, ke = min(K, kb + ks);
   uint32_t phase = 0;
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  // register stage (next chunk prefetched under the current MMAs): thread t
+  // holds column t of X^T (= X[k][t]) and columns t, t+128 of dY
+  float xa[TC_KC], yb[2][TC_KC];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < TC_KC; ++j) {
+      const int k = k0 + j;
+      xa[j] = (t < M && k < ke) ? __ldg(A + static_cast<size_t>(k) * M + t) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int n = t + i * TC_THREADS;
+#pragma unroll
+      for (int j = 0; j < TC_KC; ++j) {
+        const int k = k0 + j;
+        yb[i][j] = (n < NP && k < ke) ? __ldg(B + static_cast<size_t>(k) * N + n) : 0.f;
+      }
+    }
+  };
+  load_chunk(kb);
   for (int k0 = kb; k0 < ke; k0 += TC_KC) {
     // A^T chunk: thread t = output row m, 4 K rows per float4 (K-major cores)
 #pragma unroll
     for (int kc = 0; kc < TC_KC / 4; ++kc) {
-      float w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int k = k0 + kc * 4 + j;
-        w[j] = (t < M && k < ke) ? A[static_cast<size_t>(k) * M + t] : 0.f;
-      }
       float4 h, l;
-      split_tf32(w[0], h.x, l.x);
-      split_tf32(w[1], h.y, l.y);
-      split_tf32(w[2], h.z, l.z);
-      split_tf32(w[3], h.w, l.w);
+      split_tf32(xa[kc * 4 + 0], h.x, l.x);
+      split_tf32(xa[kc * 4 + 1], h.y, l.y);
+      split_tf32(xa[kc * 4 + 2], h.z, l.z);
+      split_tf32(xa[kc * 4 + 3], h.w, l.w);
       const int off = (kc * 16 + t / 8) * 32 + (t % 8) * 4;
       *reinterpret_cast<float4*>(a_hi + off) = h;
       *reinterpret_cast<float4*>(a_lo + off) = l;
     }
     // dY chunk: column n of B, 4 K rows per float4 (same layout as the NN kernel)
-    for (int n = t; n < NP; n += TC_THREADS) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int n = t + i * TC_THREADS;
+      if (n >= NP) continue;
 #pragma unroll
       for (int kc = 0; kc < TC_KC / 4; ++kc) {
-        float w[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + kc * 4 + j;
-          w[j] = (k < ke) ? B[static_cast<size_t>(k) * N + n] : 0.f;
-        }
         float4 h, l;
-        split_tf32(w[0], h.x, l.x);
-        split_tf32(w[1], h.y, l.y);
-        split_tf32(w[2], h.z, l.z);
-        split_tf32(w[3], h.w, l.w);
+        split_tf32(yb[i][kc * 4 + 0], h.x, l.x);
+        split_tf32(yb[i][kc * 4 + 1], h.y, l.y);
+        split_tf32(yb[i][kc * 4 + 2], h.z, l.z);
+        split_tf32(yb[i][kc * 4 + 3], h.w, l.w);
         const int off = (kc * (NP / 8) + n / 8) * 32 + (n % 8) * 4;
         *reinterpret_cast<float4*>(b_hi + off) = h;
         *reinterpret_cast<float4*>(b_lo + off) = l;
@@ -346,6 +357,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3)
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(&mbar)) : "memory");
     }
+    if (k0 + TC_KC < ke) load_chunk(k0 + TC_KC);  // in flight under the MMAs
     mbar_wait(smem_u32(&mbar), phase);
     phase ^= 1;
   }

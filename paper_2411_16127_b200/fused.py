@@ -239,10 +239,10 @@ def gemm(A, B, trans_a=False, out=None, accumulate=False, stream=None):
     return out
 
 
-def gat_logits(Hf, a_l, a_r, heads, head_dim, stream=None):
+def gat_logits(Hf, a_l, a_r, heads, head_dim, stream=None, el=None, er=None):
     n = Hf.shape[0]
-    el = torch.empty(n, heads, dtype=Hf.dtype, device=Hf.device)
-    er = torch.empty_like(el)
+    el = torch.empty(n, heads, dtype=Hf.dtype, device=Hf.device) if el is None else el
+    er = torch.empty_like(el) if er is None else er
     check(lib().gf_gat_logits(DTYPES[Hf.dtype], n, heads, head_dim, _p(Hf), _p(a_l), _p(a_r),
                               _p(el), _p(er), _stream(stream)), "gf_gat_logits")
     return el, er
