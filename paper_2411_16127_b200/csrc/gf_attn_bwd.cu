@@ -94,7 +94,12 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const int c = lane % LPE, sub = lane / LPE;
   // nrows consecutive warp rows, software-pipelined like fwd_row (gf_attn_fwd.cu)
   const int4 zero4 = make_int4(0, 0, 0, 0);
+#if GF_SCHED16_ROWS
   int4 rs = live ? ld_sched(a.sched + slot) : zero4;
+#else
+  const int v0 = live ? __ldg(a.order + slot) : 0;
+  int4 rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
+#endif
   int4 rsn = nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
   int nxt = 0;
   for (int r = 0; r < nrows; ++r) {

@@ -56,8 +56,13 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
   const int4 zero4 = make_int4(0, 0, 0, 0);
+#if GF_SCHED16_FWD
   int4 rs = live ? ld_sched(a.sched + slot) : zero4;
-  int4 rsn = nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
+#else
+  const int v0 = live ? __ldg(a.order + slot) : 0;
+  int4 rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
+#endif
+  int4 rsn = GF_ROWPIPE && nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
   int nxt = 0;
 
   const int h = c / a.LPH;
@@ -67,8 +72,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
   const T* __restrict__ Sb = a.ES + h;        // MODE 1/2: ES[e * H + h]
 
-  for (int r = 0; r < nrows; ++r) {
-  const int4 rsnn = r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
+  for (int r = 0; r < (GF_ROWPIPE ? nrows : 1); ++r) {
+  const int4 rsnn = GF_ROWPIPE && r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
   const int v = rs.x;
   int eb = rs.y, ee = rs.z;
   if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
@@ -454,7 +459,7 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     // Short rows (average degree <= 64, e.g. ogbn-products ~26) are latency-
     // bound on their prologue: give each warp 8 consecutive rows and pipeline
     // them; long rows (Reddit ~490) keep one row per warp (A/B, profiles/).
-    a.rpw = rows_per_warp(g.e, g.n, a.pk0 - a.n_cta);
+    a.rpw = GF_ROWPIPE ? rows_per_warp(g.e, g.n, a.pk0 - a.n_cta) : 1;
     a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock * a.rpw - 1) / (kWarpsPerBlock * a.rpw);
     const int rows_per_block = kWarpsPerBlock * epw;
     const int blocks = a.n_cta + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;

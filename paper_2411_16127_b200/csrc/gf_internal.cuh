@@ -106,6 +106,19 @@ struct DevGraph {
 #ifndef GF_U_COLS
 #define GF_U_COLS 2
 #endif
+// A/B switches for the forward's row prologue (profiles/README.md).
+// First row's {node, begin, end}: 1 = one 16 B schedule-entry load, 0 = the
+// order -> pointer loads.  A/B on B200 (profiles/README.md): the forward is
+// faster with 0 (C4 2.40 -> 2.16 ms), pass A with 1 (C4 2.22 -> 2.15 ms).
+#ifndef GF_SCHED16_FWD
+#define GF_SCHED16_FWD 0
+#endif
+#ifndef GF_SCHED16_ROWS
+#define GF_SCHED16_ROWS 1
+#endif
+#ifndef GF_ROWPIPE
+#define GF_ROWPIPE 1  // software-pipelined warp rows (rows_per_warp)
+#endif
 #ifndef GF_MINB2
 #define GF_MINB2 2
 #endif
