@@ -851,9 +851,11 @@ def run_ours(args, rank, world):
     traffic = ncu_traffic(args.config, dom)
     step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D) for k in means)
     l2_peak, l2_rb = measured_l2_gather(F * 4)
-    # node tables the three kernels gather (V | Q|el | K (dot) | dO | records):
-    # the L2 denominator applies only when they fit the 126 MB L2
-    tables_bytes = 4 * n * (F + qk + (F if layer != "gat" else 0) + F + 4 * H)
+    # node tables the dominant kernel gathers (fwd / pass A: V and Q|el; pass B:
+    # dO, K (dot) and the records): the L2 denominator applies when they fit L2
+    gathered = {"fwd": F + qk, "bwd_rows": F + qk,
+                "bwd_cols": F + (F if layer != "gat" else 0) + 4 * H}
+    tables_bytes = 4 * n * gathered[dom]
 
     cpu = None
     if need_cpu:
