@@ -19,6 +19,11 @@ bool tc_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, c
                       const void* C);
 int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
             int accumulate, cudaStream_t s);
+// gf_tc_gemm_tma.cu (warp-specialised TMA + tcgen05 pipeline)
+bool tma_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, const void* A,
+                       const void* C);
+int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
+             int accumulate, cudaStream_t s);
 bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                          const void* B);
 int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
@@ -228,6 +233,13 @@ extern "C" int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int
     const char* e = std::getenv("GF_GEMM_SIMT");
     return e && e[0] == '1';
   }();
+  static const bool no_tma = [] {
+    const char* e = std::getenv("GF_GEMM_NO_TMA");
+    return e && e[0] == '1';
+  }();
+  if (!force_simt && !no_tma && gfb::tma_gemm_eligible(dtype, trans_a, M, N, K, A, C))
+    return gfb::tma_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
+                         static_cast<float*>(C), accumulate, s);
   if (!force_simt && gfb::tc_gemm_eligible(dtype, trans_a, M, N, K, A, C))
     return gfb::tc_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
                         static_cast<float*>(C), accumulate, s);

@@ -60,6 +60,9 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   lo = x - hi;
+#if GF_TF32_RAW_HI  // experiment: hand the tensor core the raw fp32 as "hi"
+  hi = x;
+#endif
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
