@@ -1,3 +1,7 @@
+#pragma once
+// (Included by gf_attn_bwd_f32.cu / gf_attn_bwd_f64.cu, one translation unit
+// per element type, compiled in parallel.)
+//
 // Recompute backward of the fused AT-GNN layer for sm_100a.  Replaces the
 // reference's serial backward_values (autograd.hpp:158-170) =
 // spmm_backward (33-58) -> softmax_backward (62-73) -> sddmm_backward
@@ -724,8 +728,5 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   }
   return GF_OK;
 }
-
-template int launch_bwd<float>(const DevGraph&, BwdArgs<float>, int, int, cudaStream_t);
-template int launch_bwd<double>(const DevGraph&, BwdArgs<double>, int, int, cudaStream_t);
 
 }  // namespace gfb

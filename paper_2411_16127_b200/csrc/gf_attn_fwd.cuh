@@ -1,3 +1,8 @@
+#pragma once
+// (Included by gf_attn_fwd_f32.cu / gf_attn_fwd_f64.cu: one translation unit
+// per element type so the two halves of the kernel instantiations compile in
+// parallel.)
+//
 // Fused AT-GNN forward for sm_100a: SDDMM -> per-destination edge softmax ->
 // SpMM in ONE launch, scores and softmax statistics kept in registers (warp
 // rows) or registers + shared memory (CTA rows).  Replaces the reference's
@@ -398,6 +403,7 @@ int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cuda
 
 }  // namespace
 
+#ifdef GF_FWD_PRIMARY  // non-template definitions: emitted by the f32 unit only
 FastShape fast_shape(int H, int D, int elem_bytes) {
   FastShape f;
   if (H < 1 || D < 1) return f;
@@ -418,6 +424,8 @@ FastShape fast_shape(int H, int D, int elem_bytes) {
   f.lpe = static_cast<int>(lpe);
   return f;
 }
+
+#endif  // GF_FWD_PRIMARY
 
 static bool aligned(const void* p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; }
 
@@ -520,15 +528,5 @@ int launch_materialize_p(const DevGraph& g, const FwdArgs<T>& a, int variant, T*
   GF_CHECK_LAUNCH("materialize_p");
   return GF_OK;
 }
-
-template int launch_fwd<float>(const DevGraph&, const FwdArgs<float>&, int, cudaStream_t);
-template int launch_fwd_mode<float>(const DevGraph&, const FwdArgs<float>&, int, int, cudaStream_t);
-template int launch_fwd_mode<double>(const DevGraph&, const FwdArgs<double>&, int, int,
-                                     cudaStream_t);
-template int launch_fwd<double>(const DevGraph&, const FwdArgs<double>&, int, cudaStream_t);
-template int launch_materialize_p<float>(const DevGraph&, const FwdArgs<float>&, int, float*,
-                                         cudaStream_t);
-template int launch_materialize_p<double>(const DevGraph&, const FwdArgs<double>&, int, double*,
-                                          cudaStream_t);
 
 }  // namespace gfb
