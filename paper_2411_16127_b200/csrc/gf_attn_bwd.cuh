@@ -23,7 +23,7 @@
 //       dV[u] += p dO[v];  dot: dQ[u] += scale dS Khat[v]
 //                          add: del[u] += dS lrelu'(pre)
 // AGNN's L2 Jacobian is applied in each pass's epilogue on the owned row.
-// Scheduling and lane mapping mirror the forward (gf_attn_fwd.cu).
+// Scheduling and lane mapping mirror the forward (gf_attn_fwd.cuh).
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 
@@ -96,7 +96,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
-  // nrows consecutive warp rows, software-pipelined like fwd_row (gf_attn_fwd.cu)
+  // nrows consecutive warp rows, software-pipelined like fwd_row (gf_attn_fwd.cuh)
   const int4 zero4 = make_int4(0, 0, 0, 0);
 #if GF_SCHED16_ROWS
   int4 rs = live ? ld_sched(a.sched + slot) : zero4;

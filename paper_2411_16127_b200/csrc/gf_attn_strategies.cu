@@ -5,7 +5,7 @@
 // only its counter model (engine.hpp:84-168) tells them apart; here each one
 // has the launch structure and HBM traffic that model describes:
 //
-//   SMMF      1 launch : fwd_fast MODE 0 (gf_attn_fwd.cu) — scores, softmax
+//   SMMF      1 launch : fwd_fast MODE 0 (gf_attn_fwd.cuh) — scores, softmax
 //                        and aggregation fused, nothing E x H in HBM.
 //   PMF       2 launches: sddmm_edges (edge-parallel, the reference's
 //                        edge_parallel_partition balance, schedule.cpp:62-77)

@@ -186,7 +186,7 @@ struct BwdArgs {
   int rpw = 1;               // warp-bucket rows per warp
 };
 
-// Launchers (defined in gf_attn_fwd.cu / gf_attn_bwd.cu).
+// Launchers (defined in gf_attn_fwd.cuh / gf_attn_bwd.cuh).
 template <typename T>
 int launch_fwd(const DevGraph& g, const FwdArgs<T>& a, int variant, cudaStream_t s);
 template <typename T>
