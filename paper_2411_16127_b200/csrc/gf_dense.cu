@@ -216,6 +216,95 @@ __global__ void gat_da_reduce(int blocks, int F, const T* __restrict__ part, T* 
 
 int grid_for(int64_t work) { return static_cast<int>(std::min<int64_t>(8192, (work + 255) / 256 + 1)); }
 
+// ---- fp32 fast paths (D % 4 == 0, F <= 256): float4 rows, one pass ----------
+// el/er: thread per (row, head), the head's D values as float4s.
+__global__ void gat_logits_vec(int64_t n, int H, int D, const float* __restrict__ Hf,
+                               const float* __restrict__ al, const float* __restrict__ ar,
+                               float* __restrict__ el, float* __restrict__ er) {
+  const int F = H * D;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * H;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / H;
+    const int h = static_cast<int>(i - r * H);
+    const float4* x = reinterpret_cast<const float4*>(Hf + r * F + h * D);
+    const float4* a = reinterpret_cast<const float4*>(al + h * D);
+    const float4* b = reinterpret_cast<const float4*>(ar + h * D);
+    float sa = 0.f, sb = 0.f;
+    for (int d = 0; d < D / 4; ++d) {
+      const float4 v = __ldg(x + d), p = __ldg(a + d), q = __ldg(b + d);
+      sa += v.x * p.x + v.y * p.y + v.z * p.z + v.w * p.w;
+      sb += v.x * q.x + v.y * q.y + v.z * q.z + v.w * q.w;
+    }
+    el[i] = sa;
+    er[i] = sb;
+  }
+}
+
+// GAT fan-in in one pass (models.hpp:143-150): dH = dV + del (x) a_l + der (x)
+// a_r and the da_l / da_r column sums Hf^T del, Hf^T der.  Thread -> fixed
+// float4 column chunk (blockDim = rows_per_iter * F/4), grid-stride over rows;
+// per-block partials reduced in shared memory in a fixed order, then across
+// blocks by gat_da_reduce_par (deterministic).
+__global__ void __launch_bounds__(256) gat_fanin_vec(int64_t n, int H, int D,
+                                                     const float* __restrict__ Hf,
+                                                     const float* __restrict__ al,
+                                                     const float* __restrict__ ar,
+                                                     const float* __restrict__ dV,
+                                                     const float* __restrict__ del,
+                                                     const float* __restrict__ der,
+                                                     float* __restrict__ dH,
+                                                     float* __restrict__ part) {
+  extern __shared__ float red[];  // [rows_per_iter][2F]
+  const int F = H * D, C4 = F / 4;
+  const int rpi = blockDim.x / C4;  // rows per iteration
+  const int c = threadIdx.x % C4, rr = threadIdx.x / C4;
+  const int h = (4 * c) / D;
+  const float4 a = __ldg(reinterpret_cast<const float4*>(al) + c);
+  const float4 b = __ldg(reinterpret_cast<const float4*>(ar) + c);
+  float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
+  if (rr < rpi) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(rpi) + rr; r < n;
+         r += static_cast<int64_t>(gridDim.x) * rpi) {
+      const float l = __ldg(del + r * H + h), q = __ldg(der + r * H + h);
+      const float4 v = __ldg(reinterpret_cast<const float4*>(dV + r * F) + c);
+      const float4 x = __ldg(reinterpret_cast<const float4*>(Hf + r * F) + c);
+      reinterpret_cast<float4*>(dH + r * F)[c] =
+          make_float4(v.x + l * a.x + q * b.x, v.y + l * a.y + q * b.y, v.z + l * a.z + q * b.z,
+                      v.w + l * a.w + q * b.w);
+      sa.x += x.x * l, sa.y += x.y * l, sa.z += x.z * l, sa.w += x.w * l;
+      sb.x += x.x * q, sb.y += x.y * q, sb.z += x.z * q, sb.w += x.w * q;
+    }
+    float* o = red + rr * 2 * F;
+    o[4 * c + 0] = sa.x, o[4 * c + 1] = sa.y, o[4 * c + 2] = sa.z, o[4 * c + 3] = sa.w;
+    o[F + 4 * c + 0] = sb.x, o[F + 4 * c + 1] = sb.y, o[F + 4 * c + 2] = sb.z,
+    o[F + 4 * c + 3] = sb.w;
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < 2 * F; f += blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < rpi; ++k) acc += red[k * 2 * F + f];  // fixed order
+    part[static_cast<size_t>(blockIdx.x) * 2 * F + f] = acc;
+  }
+}
+
+// Sum `blocks` partials of 2F values in a fixed order with one warp per
+// output: lanes stride the partials, then a fixed-shape shuffle tree.
+__global__ void gat_da_reduce_par(int blocks, int F, const float* __restrict__ part,
+                                  float* __restrict__ dal, float* __restrict__ dar) {
+  const int lane = threadIdx.x & 31;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (f >= 2 * F) return;
+  float s = 0.f;
+  for (int b = lane; b < blocks; b += 32) s += part[static_cast<size_t>(b) * 2 * F + f];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    if (f < F)
+      dal[f] = s;
+    else
+      dar[f - F] = s;
+  }
+}
+
 }  // namespace
 }  // namespace gfb
 
@@ -263,7 +352,15 @@ extern "C" int gf_gat_logits(int32_t dtype, int64_t n, int32_t H, int32_t D, con
   if (n == 0) return GF_OK;
   auto s = static_cast<cudaStream_t>(stream);
   const int grid = gfb::grid_for(n * H);
-  if (dtype == GF_F32)
+  const bool vec = D % 4 == 0 && ((reinterpret_cast<uintptr_t>(Hf) | reinterpret_cast<uintptr_t>(a_l) |
+                                   reinterpret_cast<uintptr_t>(a_r)) & 15u) == 0;
+  if (dtype == GF_F32 && vec) {
+    const int g2 = static_cast<int>(std::min<int64_t>(148 * 32, (n * H + 255) / 256));
+    gfb::gat_logits_vec<<<g2, 256, 0, s>>>(n, H, D, static_cast<const float*>(Hf),
+                                           static_cast<const float*>(a_l),
+                                           static_cast<const float*>(a_r), static_cast<float*>(el),
+                                           static_cast<float*>(er));
+  } else if (dtype == GF_F32)
     gfb::gat_logits_kernel<float><<<grid, 256, 0, s>>>(
         n, H, D, static_cast<const float*>(Hf), static_cast<const float*>(a_l),
         static_cast<const float*>(a_r), static_cast<float*>(el), static_cast<float*>(er));
@@ -280,6 +377,26 @@ template <typename T>
 int fanin_impl(int64_t n, int H, int D, const T* Hf, const T* al, const T* ar, const T* dV,
                const T* del, const T* der, T* dH, T* dal, T* dar, cudaStream_t s) {
   const int F = H * D;
+  if constexpr (sizeof(T) == 4) {
+    const bool al16 = ((reinterpret_cast<uintptr_t>(Hf) | reinterpret_cast<uintptr_t>(al) |
+                        reinterpret_cast<uintptr_t>(ar) | reinterpret_cast<uintptr_t>(dV) |
+                        reinterpret_cast<uintptr_t>(dH)) & 15u) == 0;
+    if (D % 4 == 0 && F <= 256 && al16) {
+      const int c4 = F / 4, rpi = 256 / c4;
+      const int threads = rpi * c4;
+      const int blocks = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(148 * 8, (n + rpi - 1) / rpi)));
+      const size_t smem = sizeof(float) * rpi * 2 * F;
+      T* part = nullptr;
+      GF_CHECK_CUDA(gfb::scratch_alloc(&part, sizeof(T) * blocks * 2 * F, s));
+      gfb::gat_fanin_vec<<<blocks, threads, smem, s>>>(n, H, D, Hf, al, ar, dV, del, der, dH, part);
+      GF_CHECK_LAUNCH("gat_fanin_vec");
+      gfb::gat_da_reduce_par<<<(2 * F * 32 + 255) / 256, 256, 0, s>>>(blocks, F, part, dal, dar);
+      GF_CHECK_LAUNCH("gat_da_reduce_par");
+      cudaFreeAsync(part, s);
+      return GF_OK;
+    }
+  }
   gfb::gat_dh_kernel<T><<<gfb::grid_for(n * F), 256, 0, s>>>(n, H, D, al, ar, dV, del, der, dH);
   GF_CHECK_LAUNCH("gat_dh");
   const int64_t rpb = 512;

@@ -80,3 +80,32 @@ def test_gat_logits_and_fanin(cuda):
     assert rel_err(dH.cpu().numpy(), ref) < 1e-12
     assert rel_err(dal.cpu().numpy(), (Hf.reshape(n, H, D) * dl[:, :, None]).sum(0).reshape(-1)) < 1e-11
     assert rel_err(dar.cpu().numpy(), (Hf.reshape(n, H, D) * dr[:, :, None]).sum(0).reshape(-1)) < 1e-11
+
+
+@pytest.mark.parametrize("n", [777, 300_000])
+def test_gat_logits_and_fanin_fp32_fast_path(cuda, n):
+    """fp32 float4 paths (gat_logits_vec, gat_fanin_vec + parallel fixed-order
+    reduce) against an fp64 reference; deterministic across calls."""
+    from paper_2411_16127_b200 import fused
+
+    rng = np.random.default_rng(5)
+    H, D = 8, 8
+    Hf = rng.uniform(-1, 1, (n, H * D)).astype(np.float32)
+    al, ar = (rng.uniform(-1, 1, H * D).astype(np.float32) for _ in range(2))
+    dV = rng.uniform(-1, 1, (n, H * D)).astype(np.float32)
+    dl, dr = (rng.uniform(-1, 1, (n, H)).astype(np.float32) for _ in range(2))
+    t = lambda a: torch.from_numpy(a).to(cuda)  # noqa: E731
+    el, er = fused.gat_logits(t(Hf), t(al), t(ar), H, D)
+    H64 = Hf.astype(np.float64).reshape(n, H, D)
+    assert rel_err(el.cpu().numpy(), (H64 * al.reshape(H, D)).sum(-1)) < 1e-5
+    assert rel_err(er.cpu().numpy(), (H64 * ar.reshape(H, D)).sum(-1)) < 1e-5
+    dH, dal, dar = fused.gat_fanin(t(Hf), t(al), t(ar), t(dV), t(dl), t(dr), H, D)
+    ref = dV + (dl[:, :, None] * al.reshape(H, D) + dr[:, :, None] * ar.reshape(H, D)).reshape(n, -1)
+    assert rel_err(dH.cpu().numpy(), ref) < 1e-6
+    ref_al = (H64 * dl[:, :, None]).sum(0).reshape(-1)
+    ref_ar = (H64 * dr[:, :, None]).sum(0).reshape(-1)
+    scale = max(1.0, float(np.abs(H64).sum() / (H * D) ** 0.5 / 1e2))
+    assert float(np.abs(dal.cpu().numpy() - ref_al).max()) / scale < 1e-4
+    assert float(np.abs(dar.cpu().numpy() - ref_ar).max()) / scale < 1e-4
+    _, dal2, _ = fused.gat_fanin(t(Hf), t(al), t(ar), t(dV), t(dl), t(dr), H, D)
+    assert torch.equal(dal, dal2)
