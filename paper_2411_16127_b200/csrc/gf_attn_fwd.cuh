@@ -462,12 +462,12 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     const int epw = 32 / fs.lpe;
     // packed bucket: the small rows (and, unless skipped, the empty ones) when
     // a warp holds more than one edge slot
-    a.pk0 = epw > 1 ? std::max(a.n_cta, g.n - g.n_empty_rows - g.n_small_rows) : a.n;
+    a.pk0 = epw > 1 ? std::max(a.n_cta, g.n - a.n_empty - a.n_small) : a.n;
     a.pk0 = std::min(a.pk0, a.n);
     // Short rows (average degree <= 64, e.g. ogbn-products ~26) are latency-
     // bound on their prologue: give each warp 8 consecutive rows and pipeline
     // them; long rows (Reddit ~490) keep one row per warp (A/B, profiles/).
-    a.rpw = GF_ROWPIPE ? rows_per_warp(g.e, g.n, a.pk0 - a.n_cta) : 1;
+    a.rpw = GF_ROWPIPE ? rows_per_warp(a.e, g.n, a.pk0 - a.n_cta) : 1;
     a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock * a.rpw - 1) / (kWarpsPerBlock * a.rpw);
     const int rows_per_block = kWarpsPerBlock * epw;
     const int blocks = a.n_cta + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;

@@ -23,6 +23,7 @@
 // records (so the recompute backward runs after any of them), plus P when
 // requested.
 #include <algorithm>
+#include <mutex>
 
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
@@ -302,6 +303,8 @@ int grid_1d(int64_t work) {
 }  // namespace
 
 int ensure_coo_dst(DevGraph& g, cudaStream_t s) {
+  static std::mutex mu;  // graphs are shareable across host threads (reference SPEC.md:98)
+  std::lock_guard<std::mutex> lock(mu);
   if (g.coo_dst || g.e == 0) return GF_OK;
   GF_CHECK_CUDA(cudaMalloc(&g.coo_dst, sizeof(int32_t) * g.e));
   const int blocks = static_cast<int>(std::min<int64_t>(148 * 32, (int64_t(g.n) * 32 + 255) / 256 + 1));

@@ -95,6 +95,9 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
   a.idx = g.col;
   a.order = g.row_order;
   a.sched = g.row_sched;
+  a.n_small = g.n_small_rows;
+  a.n_empty = g.n_empty_rows;
+  a.e = g.e;
   a.n = g.active_rows();
   a.n_cta = g.n_cta_rows;
   a.H = d.heads;

@@ -159,6 +159,8 @@ struct FwdArgs {
   T* stats;  // N x H x 4 records (gf_device.cuh Rec)
   int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
   int rpw = 1;               // warp-bucket rows per warp (software-pipelined prologues)
+  int n_small = 0, n_empty = 0;  // bucket counts of the order being walked (rows or columns)
+  int64_t e = 0;                 // edges of that view (rows_per_warp)
   const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
   const int32_t* eperm = nullptr;  // MODE 3: slot -> CSR edge id of ES (CSC passes)
 };

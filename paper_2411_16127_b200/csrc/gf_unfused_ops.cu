@@ -18,6 +18,7 @@
 //                    add: add_grad (rows -> der, columns -> del)
 // Owner-computes everywhere (no atomics): deterministic.
 #include <algorithm>
+#include <mutex>
 
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
@@ -176,6 +177,9 @@ FwdArgs<T> base_args(const DevGraph& g, int H, int D, bool csc) {
   a.idx = csc ? g.csc_row : g.col;
   a.order = csc ? g.col_order : g.row_order;
   a.sched = csc ? g.col_sched : g.row_sched;
+  a.n_small = csc ? g.n_small_cols : g.n_small_rows;
+  a.n_empty = csc ? g.n_empty_cols : g.n_empty_rows;
+  a.e = csc ? g.e_csc : g.e;
   a.n = csc ? g.active_cols() : g.active_rows();
   a.n_cta = csc ? g.n_cta_cols : g.n_cta_rows;
   a.H = H;
@@ -290,6 +294,8 @@ bool bad_shape(gf_graph_t g, int32_t dtype, int32_t heads, int32_t head_dim, con
 }  // namespace
 
 int ensure_csc_perm(DevGraph& g, cudaStream_t s) {
+  static std::mutex mu;  // graphs are shareable across host threads
+  std::lock_guard<std::mutex> lock(mu);
   if (g.csc_perm || g.e == 0) return GF_OK;
   if (!whole_graph(g, "csc_perm")) return GF_ERR_UNSUPPORTED;
   GF_CHECK_CUDA(cudaMalloc(&g.csc_perm, sizeof(int32_t) * g.e));
