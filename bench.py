@@ -86,22 +86,8 @@ def gen_graph_device(name, device, seed=0):
         # 1024 molecules of 26 atoms: a random spanning tree + 3 ring bonds,
         # bonds in both directions (~25.5 atoms / 27.5 bonds per ogbg-molhiv graph).
         mols, atoms = 1024, 26
-        rng = np.random.default_rng(seed)
-        s_all, d_all = [], []
-        for m in range(mols):
-            base = m * atoms
-            parent = [rng.integers(0, i) for i in range(1, atoms)]
-            a = [base + i for i in range(1, atoms)] + [base + x for x in rng.integers(0, atoms, 3)]
-            b = [base + p for p in parent] + [base + x for x in rng.integers(0, atoms, 3)]
-            s_all += a + b
-            d_all += b + a
-        n = mols * atoms
-        src = torch.tensor(s_all, device=device)
-        dst = torch.tensor(d_all, device=device)
-        keep = src != dst
-        src, dst = src[keep], dst[keep]
-        key = torch.unique(dst.to(torch.int64) * n + src.to(torch.int64))
-        return n, key % n, key // n
+        src, dst = fused.gen_molecules_device(mols, atoms, 3, seed=seed, device=device)
+        return mols * atoms, src, dst
     raise ValueError(name)
 
 

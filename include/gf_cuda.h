@@ -248,12 +248,19 @@ int gf_gat_fanin(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf,
  *                edges with destinations != 0
  *   power_law  : row r of deg_r = round(max_degree (r+1)^-exponent) is a
  *                hashed node id, sources uniform, duplicate sources dropped
- *                (capacity >= sum deg_r) */
+ *                (capacity >= sum deg_r)
+ *   molecules  : `mols` disjoint blocks of `atoms` ids (the batch_graphs
+ *                layout, graph.cpp:104-118), each a random spanning tree plus
+ *                `rings` extra bonds, both directions, no self-loops or
+ *                duplicates (capacity >= 2 mols (atoms - 1 + rings)) */
 int gf_gen_random_device(int64_t n, double avg_degree, uint64_t seed, int64_t* src, int64_t* dst,
                          int64_t* e_out, void* stream);
 int gf_gen_super_node_device(int64_t n, double avg_degree, int64_t hub_degree, uint64_t seed,
                              int64_t* src, int64_t* dst, int64_t* e_out, void* stream);
 int gf_gen_power_law_device(int64_t n, int64_t max_degree, double exponent, uint64_t seed,
+                            int64_t capacity, int64_t* src, int64_t* dst, int64_t* e_out,
+                            void* stream);
+int gf_gen_molecules_device(int64_t mols, int64_t atoms, int64_t rings, uint64_t seed,
                             int64_t capacity, int64_t* src, int64_t* dst, int64_t* e_out,
                             void* stream);
 

@@ -330,3 +330,73 @@ extern "C" int gf_gen_super_node_device(int64_t n, double avg_degree, int64_t hu
   gfb::set_error("gf_gen_super_node_device: could not draw enough distinct edges");
   return GF_ERR_GRAPH;
 }
+
+namespace gfb {
+namespace {
+// molecule m, bond j: j < atoms-1 is the tree bond (atom j+1 -> a hashed
+// parent < j+1, so every molecule is connected), the rest are ring bonds
+// between two hashed atoms; both directions, self-loops rejected.
+__global__ void molecule_candidates(uint64_t seed, int64_t mols, int64_t atoms, int64_t rings,
+                                    uint64_t* __restrict__ keys) {
+  const int64_t per = atoms - 1 + rings, count = mols * per;
+  const uint64_t n = static_cast<uint64_t>(mols * atoms);
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < count;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = c / per, j = c % per;
+    const uint64_t h1 = mix64(seed ^ mix64(0x6D6F6Cull + 2 * static_cast<uint64_t>(c)));
+    const uint64_t h2 = mix64(seed ^ mix64(0x6D6F6Cull + 2 * static_cast<uint64_t>(c) + 1));
+    uint64_t a, b;
+    if (j < atoms - 1) {
+      a = static_cast<uint64_t>(j + 1);
+      b = static_cast<uint64_t>((static_cast<unsigned __int128>(h1) * a) >> 64);
+    } else {
+      a = static_cast<uint64_t>((static_cast<unsigned __int128>(h1) * atoms) >> 64);
+      b = static_cast<uint64_t>((static_cast<unsigned __int128>(h2) * atoms) >> 64);
+    }
+    const uint64_t base = static_cast<uint64_t>(m * atoms);
+    const bool loop = a == b;
+    keys[2 * c] = loop ? ~0ull : (base + b) * n + (base + a);
+    keys[2 * c + 1] = loop ? ~0ull : (base + a) * n + (base + b);
+  }
+}
+}  // namespace
+}  // namespace gfb
+
+// Batched molecules (the C2 ogbg-molhiv shape; the device counterpart of
+// batch_graphs over per-molecule graphs, graph.cpp:104-118): `mols` disjoint
+// blocks of `atoms` ids, each a random spanning tree plus `rings` extra bonds,
+// every bond in both directions, duplicates and self-loops removed.
+// capacity >= 2 * mols * (atoms - 1 + rings); *e_out = edges written.
+extern "C" int gf_gen_molecules_device(int64_t mols, int64_t atoms, int64_t rings, uint64_t seed,
+                                       int64_t capacity, int64_t* src, int64_t* dst,
+                                       int64_t* e_out, void* stream) {
+  if (mols <= 0 || atoms <= 0 || rings < 0 || !e_out || mols > (int64_t(1) << 31) / atoms) {
+    gfb::set_error("gf_gen_molecules_device: invalid arguments");
+    return GF_ERR_INVALID;
+  }
+  const int64_t cand = 2 * mols * (atoms - 1 + rings), n = mols * atoms;
+  if (cand > capacity) {
+    gfb::set_error("gf_gen_molecules_device: capacity below 2 * mols * (atoms - 1 + rings)");
+    return GF_ERR_INVALID;
+  }
+  *e_out = 0;
+  if (cand == 0) return GF_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  uint64_t *keys = nullptr, *tmp = nullptr, *uniq = nullptr;
+  GF_CHECK_CUDA(gfb::scratch_alloc(&keys, sizeof(uint64_t) * cand, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&tmp, sizeof(uint64_t) * cand, s));
+  GF_CHECK_CUDA(gfb::scratch_alloc(&uniq, sizeof(uint64_t) * cand, s));
+  gfb::molecule_candidates<<<gfb::grid_of(cand / 2), 256, 0, s>>>(seed, mols, atoms, rings, keys);
+  int rc = cudaGetLastError() == cudaSuccess ? GF_OK : GF_ERR_CUDA;
+  int64_t have = 0;
+  if (!rc) rc = gfb::sort_unique(keys, tmp, cand, uniq, &have, s);
+  if (!rc && have > 0) {
+    gfb::unpack_coo<<<gfb::grid_of(have), 256, 0, s>>>(uniq, have, n, src, dst);
+    if (cudaGetLastError() != cudaSuccess) rc = GF_ERR_CUDA;
+  }
+  if (!rc) *e_out = have;
+  cudaFreeAsync(keys, s);
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(uniq, s);
+  return rc;
+}

@@ -373,3 +373,15 @@ def gen_power_law_device(n, max_degree, exponent, seed=0, device="cuda", stream=
                                         _p(dst), C.byref(out), _stream(stream)),
           "gf_gen_power_law_device")
     return src[: out.value], dst[: out.value]
+
+
+def gen_molecules_device(mols, atoms, rings, seed=0, device="cuda", stream=None):
+    """(src, dst): `mols` disjoint molecules of `atoms` ids (batch_graphs
+    layout), each a spanning tree + `rings` bonds, both directions, deduped."""
+    cap = 2 * mols * (atoms - 1 + rings)
+    src = torch.empty(max(cap, 1), dtype=torch.int64, device=device)
+    dst = torch.empty_like(src)
+    out = C.c_int64()
+    check(lib().gf_gen_molecules_device(mols, atoms, rings, seed, cap, _p(src), _p(dst),
+                                        C.byref(out), _stream(stream)), "gf_gen_molecules_device")
+    return src[: out.value], dst[: out.value]

@@ -62,3 +62,46 @@ def test_gen_power_law_device(cuda):
     # duplicate sources are dropped: each row loses at most a few edges
     assert np.all(got <= want) and np.all(want - got <= np.maximum(3, want * want // n + 3))
     assert got[0] >= mx - mx * mx // n - 5  # ~mx^2/(2n) birthday collisions
+
+
+@pytest.mark.parametrize("mols,atoms,rings", [(1024, 26, 3), (7, 1, 0), (5, 2, 4), (300, 40, 0)])
+def test_gen_molecules_device(cuda, mols, atoms, rings):
+    from paper_2411_16127_b200 import fused
+
+    src, dst = fused.gen_molecules_device(mols, atoms, rings, seed=3)
+    n = mols * atoms
+    s, d = src.cpu().numpy(), dst.cpu().numpy()
+    k = d * n + s
+    assert len(np.unique(k)) == len(k) and np.all(np.diff(k) > 0)  # distinct, (dst, src) order
+    assert not np.any(s == d)  # no self-loops
+    assert np.all(s // atoms == d // atoms)  # block diagonal (batch_graphs layout)
+    assert set((d * n + s).tolist()) == set((s * n + d).tolist())  # both directions
+    assert 2 * mols * (atoms - 1) <= len(k) <= 2 * mols * (atoms - 1 + rings)
+    if rings == 0:  # a tree per molecule: exactly atoms-1 undirected bonds
+        assert len(k) == 2 * mols * (atoms - 1)
+    # every molecule connected: union-find over the bonds
+    parent = np.arange(n)
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for a, b in zip(s.tolist(), d.tolist()):
+        ra, rb = find(a), find(b)
+        if ra != rb:
+            parent[ra] = rb
+    roots = np.array([find(i) for i in range(n)])
+    assert len(np.unique(roots)) == mols
+    s2, d2 = fused.gen_molecules_device(mols, atoms, rings, seed=3)
+    assert torch.equal(src, s2) and torch.equal(dst, d2)
+    row_ptr, _, _, _, _ = fused.from_coo_device(n, src, dst)
+    assert int(row_ptr[-1]) == len(k)
+
+
+def test_gen_molecules_device_errors(cuda):
+    from paper_2411_16127_b200 import fused
+
+    with pytest.raises(Exception, match="gen_molecules"):
+        fused.gen_molecules_device(0, 26, 3)
