@@ -194,6 +194,37 @@ def measured_l2_gather(row_bytes, footprint=64 << 20):
     return g.value, rb
 
 
+def l2_request_costs():
+    """Per-request L2 gather costs (ps) fitted live from two probe points:
+    a random 32 B row is one line + one sector, a 128 B row one line + four
+    sectors (t = a*lines + b*sectors).  The 256 B point checks the fit."""
+    g32, _ = measured_l2_gather(32)
+    g128, _ = measured_l2_gather(128)
+    t32, t128 = 32 / g32 * 1e3, 128 / g128 * 1e3  # ps per row
+    b = (t128 - t32) / 3
+    return t32 - b, b, g32, g128
+
+
+def gathered_rows(kernel, layer, H, D, b=4):
+    """Row sizes (bytes) each edge gathers in one launch."""
+    F = H * D
+    rec = 16 * H if b == 4 else 32 * H
+    if layer == "gat":
+        return {"fwd": [b * F, b * H], "bwd_rows": [b * F, b * H], "bwd_cols": [b * F, rec]}[kernel]
+    return {"fwd": [b * F, b * F], "bwd_rows": [b * F, b * F],
+            "bwd_cols": [b * F, b * F, rec]}[kernel]
+
+
+def l2_request_model_ms(kernel, layer, H, D, e, a_ps, b_ps):
+    """Modelled launch time when every gather is an L2 hit: per edge and
+    gathered row, a line-request cost per 128 B line touched plus a sector
+    cost per 32 B sector."""
+    t = 0.0
+    for rb in gathered_rows(kernel, layer, H, D):
+        t += a_ps * max(1, -(-rb // 128)) + b_ps * max(1, -(-rb // 32))
+    return e * t * 1e-9
+
+
 def ncu_traffic(config, kernel):
     """DRAM bytes per launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -869,6 +900,8 @@ def run_ours(args, rank, world):
     traffic = ncu_traffic(args.config, dom)
     step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D) for k in means)
     l2_peak, l2_rb = measured_l2_gather(F * 4)
+    a_ps, b_ps, g32, g128 = l2_request_costs()
+    req_model = {k: l2_request_model_ms(k, layer, H, D, e_of[k], a_ps, b_ps) for k in means}
     # node tables the dominant kernel gathers (fwd / pass A: V and Q|el; pass B:
     # dO, K (dot) and the records): the L2 denominator applies when they fit L2
     gathered = {"fwd": F + qk, "bwd_rows": F + qk,
@@ -920,6 +953,15 @@ def run_ours(args, rank, world):
                             "step_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / l2_peak,
                             "peak_kind": f"measured live: gf_measure_l2_gather, {l2_rb} B rows "
                                          "(the gathered row size), 64 MiB L2-resident footprint"},
+            "l2_request_model": {
+                "kernel_frac": {k: round(req_model[k] / means[k], 4) for k in means},
+                "step_frac": sum(req_model.values()) / (ms_per_step),
+                "model_ms": {k: round(v, 4) for k, v in req_model.items()},
+                "line_ps": a_ps, "sector_ps": b_ps, "probe_gbs": {"32": g32, "128": g128},
+                "applies": tables_bytes <= L2_BYTES,
+                "note": "t = E * sum over gathered rows (line_ps * 128 B lines + sector_ps * "
+                        "32 B sectors), costs fitted live from the 32 B and 128 B L2 probe "
+                        "points: the ceiling for request-bound gathers from L2-resident tables"},
             "step_roofline": {"algorithmic_bytes": step_bytes,
                               "achieved": step_bytes / (ms_per_step / 1e3) / 1e9,
                               "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},
