@@ -14,6 +14,7 @@
 //    (src,dst) sort — bit-exact with graph.cpp:25-57.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <vector>
 
 #include "gf_device.cuh"
@@ -158,16 +159,15 @@ void free_graph(DevGraph* g) {
 // ------------------------------------------------------- device from_coo --
 __global__ void coo_check_pack(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
                                int64_t e, int64_t n, int b, uint64_t* __restrict__ k_ds,
-                               uint64_t* __restrict__ k_sd, unsigned long long* __restrict__ bad) {
+                               unsigned long long* __restrict__ bad) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t u = src[i], v = dst[i];
     if (u < 0 || u >= n || v < 0 || v >= n) {
       atomicMin(bad, static_cast<unsigned long long>(i));
-      k_ds[i] = k_sd[i] = 0;
+      k_ds[i] = 0;
     } else {
       k_ds[i] = (static_cast<uint64_t>(v) << b) | static_cast<uint64_t>(u);
-      k_sd[i] = (static_cast<uint64_t>(u) << b) | static_cast<uint64_t>(v);
     }
   }
 }
@@ -190,20 +190,24 @@ __global__ void unpack_sorted(const uint64_t* __restrict__ keys, int64_t e, int6
   }
 }
 
-__global__ void csc_perm_kernel(const uint64_t* __restrict__ k_ds, const uint64_t* __restrict__ k_sd,
-                                int64_t e, int b, int64_t* __restrict__ perm) {
+// CSR-sorted keys (v, u) -> swapped keys (u, v) carrying their CSR edge id:
+// sorting these pairs yields the CSC order and, in the values, csc_edge_perm
+// (CSC slot -> CSR edge id) with no search.
+__global__ void swap_with_ids(const uint64_t* __restrict__ k_ds, int64_t e, int b,
+                              uint64_t* __restrict__ k_sd, int32_t* __restrict__ ids) {
   const uint64_t mask = (1ull << b) - 1;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t u = k_sd[i] >> b, v = k_sd[i] & mask;
-    const uint64_t key = (v << b) | u;
-    int64_t lo = 0, hi = e;  // lower_bound
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (k_ds[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    perm[i] = lo;
+    const uint64_t k = k_ds[i];
+    k_sd[i] = ((k & mask) << b) | (k >> b);
+    ids[i] = static_cast<int32_t>(i);
   }
+}
+
+__global__ void widen_ids(const int32_t* __restrict__ ids, int64_t e, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = ids[i];
 }
 }  // namespace
 
@@ -349,8 +353,8 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
                                   int64_t* d_csc_ptr, int64_t* d_csc_row, int64_t* d_csc_perm,
                                   int64_t* bad, void* stream) {
   using namespace gfb;
-  if (n < 0 || e < 0 || n >= (1LL << 31)) {
-    set_error("gf_from_coo_device: invalid sizes");
+  if (n < 0 || e < 0 || n >= (1LL << 31) || e >= (1LL << 31)) {
+    set_error("gf_from_coo_device: invalid sizes (node and edge counts must fit int32)");
     return GF_ERR_INVALID;
   }
   auto s = static_cast<cudaStream_t>(stream);
@@ -369,17 +373,30 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
   int rc = GF_OK;
   unsigned long long hflags[2] = {~0ull, ~0ull};
   if (e > 0) {
-    coo_check_pack<<<grid, 256, 0, s>>>(d_src, d_dst, e, n, b, k_ds, k_sd, flags);
+    coo_check_pack<<<grid, 256, 0, s>>>(d_src, d_dst, e, n, b, k_ds, flags);
     GF_CHECK_LAUNCH("coo_check_pack");
-    size_t tb = 0;
-    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, k_ds, k_ds_s, e, 0, 2 * b, s));
+    int32_t *ids = nullptr, *ids_s = nullptr;
+    GF_CHECK_CUDA(gfb::scratch_alloc(&ids, sizeof(int32_t) * e, s));
+    GF_CHECK_CUDA(gfb::scratch_alloc(&ids_s, sizeof(int32_t) * e, s));
+    size_t tk = 0, tp = 0;
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tk, k_ds, k_ds_s, e, 0, 2 * b, s));
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tp, k_sd, k_sd_s, ids, ids_s, e, 0,
+                                                  2 * b, s));
+    const size_t tb = std::max(tk, tp);
     void* tmp = nullptr;
     GF_CHECK_CUDA(gfb::scratch_alloc(&tmp, tb, s));
     size_t t = tb;
     GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t, k_ds, k_ds_s, e, 0, 2 * b, s));
+    swap_with_ids<<<grid, 256, 0, s>>>(k_ds_s, e, b, k_sd, ids);
+    GF_CHECK_LAUNCH("swap_with_ids");
     t = tb;
-    GF_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t, k_sd, k_sd_s, e, 0, 2 * b, s));
+    GF_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k_sd, k_sd_s, ids, ids_s, e, 0, 2 * b, s));
     cudaFreeAsync(tmp, s);
+    // csc_edge_perm (graph.cpp:43-55's stable bucket scatter, as a pair sort)
+    widen_ids<<<grid, 256, 0, s>>>(ids_s, e, d_csc_perm);
+    GF_CHECK_LAUNCH("widen_ids");
+    cudaFreeAsync(ids, s);
+    cudaFreeAsync(ids_s, s);
     unpack_sorted<<<grid, 256, 0, s>>>(k_ds_s, e, n, b, d_col, d_row_ptr, flags + 1);
     GF_CHECK_LAUNCH("unpack_sorted csr");
     unpack_sorted<<<grid, 256, 0, s>>>(k_sd_s, e, n, b, d_csc_row, d_csc_ptr, flags + 1);
@@ -402,15 +419,6 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
     if (bad) *bad = -2 - static_cast<int64_t>(hflags[1]);
     set_error("from_coo: duplicate edge at sorted position " + std::to_string(hflags[1]));
     rc = GF_ERR_GRAPH;
-  }
-  if (rc == GF_OK && e > 0) {
-    // csc_edge_perm: CSR edge id of each CSC slot = position of key (v,u) in
-    // the sorted CSR keys (keys are unique once duplicates are rejected).
-    csc_perm_kernel<<<grid, 256, 0, s>>>(k_ds_s, k_sd_s, e, b, d_csc_perm);
-    if (cudaGetLastError() != cudaSuccess) {
-      set_error("launch csc_perm_kernel failed");
-      rc = GF_ERR_CUDA;
-    }
   }
   cudaFreeAsync(k_ds, s);
   cudaFreeAsync(k_sd, s);
