@@ -126,13 +126,27 @@ __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / s
   }
 }
 
+// Owned rows (read or written once per pass) may be marked evict_first so
+// they do not displace the gathered tables (GF_OWN_HINT: 1 = loads and
+// stores, 2 = stores only).
+#ifndef GF_OWN_HINT
+#define GF_OWN_HINT 0
+#endif
+
 template <typename T, int CB>
 __device__ __forceinline__ void ld_own(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
   constexpr int W = CB / sizeof(T);
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
     for (int i = 0; i < W; i += 4) {
+#if GF_OWN_HINT == 1
+      float4 v;
+      asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                   : "l"(p + i), "l"(pol_stream()));
+#else
       const float4 v = *reinterpret_cast<const float4*>(p + i);
+#endif
       x[i] = v.x, x[i + 1] = v.y, x[i + 2] = v.z, x[i + 3] = v.w;
     }
   } else {
@@ -149,8 +163,16 @@ __device__ __forceinline__ void st_chunk(T* __restrict__ p, const T (&x)[CB / si
   constexpr int W = CB / sizeof(T);
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int i = 0; i < W; i += 4)
+    for (int i = 0; i < W; i += 4) {
+#if GF_OWN_HINT
+      asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                   :: "l"(p + i), "f"(x[i]), "f"(x[i + 1]), "f"(x[i + 2]), "f"(x[i + 3]),
+                      "l"(pol_stream())
+                   : "memory");
+#else
       *reinterpret_cast<float4*>(p + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+#endif
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < W; i += 2) *reinterpret_cast<double2*>(p + i) = make_double2(x[i], x[i + 1]);
