@@ -308,6 +308,9 @@ def main():
                     help="skip the layer-level (projection + pipeline) measurement")
     ap.add_argument("--no-ablation", action="store_true",
                     help="skip the forward fusion-strategy ablation (smmf/pmf/unfused/baseline)")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="sharded training step: projected rows exchanged by the projection's own "
+                         "epilogue into symmetric memory (p2p) or by NCCL all-gather")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args()
@@ -404,6 +407,10 @@ def run_reference(args, rank, world):
     return 0
 
 
+def gat_layer(layer):
+    return layer == "gat"
+
+
 def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, shard=None):
     """One full-graph training step of the layer, fp32 (models.hpp:104-158 +
     an SGD update): projection of the owned rows (tcgen05 3xTF32), GAT
@@ -429,9 +436,24 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
     else:
         Wq, Wk = rnd(F, F), rnd(F, F)
     rows = shard.block if shard is not None else slice(0, n)
-    Hf = torch.zeros(n, F, device=dev)
-    Qb = torch.zeros(n, F, device=dev)
-    Kb = torch.zeros(n, F, device=dev)
+    # Sharded exchange of the projected rows: "p2p" = the projection's
+    # epilogue writes every rank's copy of the tables (gf_gemm_bcast into
+    # symmetric memory, device barrier); "nccl" = projection, then all-gather.
+    pt, exchange = None, None
+    if shard is not None:
+        exchange = "nccl"
+        if getattr(args, "exchange", "p2p") == "p2p":
+            try:
+                from paper_2411_16127_b200.shard import PeerTables
+
+                pt = PeerTables(shard, {"V": F} if gat_layer(layer) else {"Q": F, "K": F, "V": F},
+                                device=dev)
+                exchange = "p2p: gemm_bcast epilogue into symmetric-memory tables + device barrier"
+            except Exception as ex:  # recorded in the JSON line, NCCL path used
+                exchange = f"nccl (p2p unavailable: {type(ex).__name__}: {str(ex)[:120]})"
+    Hf = pt.table("V") if pt is not None else torch.zeros(n, F, device=dev)
+    Qb = pt.table("Q") if pt is not None and not gat_layer(layer) else torch.zeros(n, F, device=dev)
+    Kb = pt.table("K") if pt is not None and not gat_layer(layer) else torch.zeros(n, F, device=dev)
     EL = torch.zeros(n, H, device=dev)
     ER = torch.zeros(n, H, device=dev)
     O = torch.empty(n, F, device=dev)
@@ -449,7 +471,23 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
     def step(ev=None):
         rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
         rec(0)
-        if gat:
+        later = []
+        if pt is not None:
+            pt.barrier()  # every rank is done reading the previous step's tables
+            if gat:
+                fused.gemm_bcast(Xr, Wv, pt.dests("V"), stream=stream)
+                pt.barrier()
+                # el / er of every row from the complete table (deterministic per
+                # row, so identical to the owners' values): no logit exchange
+                fused.gat_logits(Hf, al, ar, H, D, stream=stream, el=EL, er=ER)
+                q, k, v = EL, ER, Hf
+            else:
+                for w_, name in ((Wq, "Q"), (Wk, "K"), (Wv, "V")):
+                    fused.gemm_bcast(Xr, w_, pt.dests(name), stream=stream)
+                pt.barrier()
+                q, k, v = Qb, Kb, Hf
+            later = [all_gather_rows(dO, shard, async_op=True)]
+        elif gat:
             fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
             fused.gat_logits(Hf[rows], al, ar, H, D, stream=stream, el=EL[rows], er=ER[rows])
             q, k, v = EL, ER, Hf
@@ -458,8 +496,7 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             fused.gemm(Xr, Wk, out=Kb[rows], stream=stream)
             fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
             q, k, v = Qb, Kb, Hf
-        later = []
-        if shard is not None:  # source rows first; dO (and K) under the forward / pass A
+        if shard is not None and pt is None:  # source rows first; dO (and K) under fwd / pass A
             for w in [all_gather_rows(t, shard, async_op=True) for t in (v, q)]:
                 w.wait()
             later = [all_gather_rows(t, shard, async_op=True)
@@ -513,6 +550,7 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             "step": "projection (+ all-gather when sharded) -> fused attention fwd + recompute "
                     "bwd -> GAT fan-in -> X^T dY (+ all-reduce when sharded) -> SGD update",
             "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; X^T*dY deterministic split-K)",
+            "exchange": exchange,
             "x_width": F}
 
 

@@ -227,6 +227,14 @@ int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q, cons
  * Row-major, fp32 or fp64; accumulate = 1 adds into C. */
 int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int64_t K, const void* A,
             const void* B, void* C, int32_t accumulate, void* stream);
+/* Projection fused with its all-gather: C = A·B (fp32,
+ * 3xTF32 tcgen05, A M x K, B K x N row-major) stored by the TMA epilogue to
+ * n_dst (1..8) row-major M x N destinations — dst[0] local, dst[1..] the
+ * same rows of the peers' tables through peer-mapped (NVLink) addresses —
+ * tile by tile.  Requires K % 4 == 0, N % 32 == 0, 16 B aligned pointers.
+ * Replaces models.hpp:116-125's projections + the row all-gather. */
+int gf_gemm_bcast(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
+                  void* const* dst, int32_t n_dst, void* stream);
 /* GAT attention logits: el[n,h] = sum_d Hf[n,h,d] a_l[h,d]; er likewise. */
 int gf_gat_logits(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf, const void* a_l,
                   const void* a_r, void* el, void* er, void* stream);

@@ -23,7 +23,7 @@ int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, flo
 bool tma_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, const void* A,
                        const void* C);
 int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
-             int accumulate, cudaStream_t s);
+             int accumulate, cudaStream_t s, float* const* peer_c = nullptr, int n_peers = 0);
 bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                          const void* B);
 int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
@@ -431,4 +431,33 @@ extern "C" int gf_gat_fanin(int32_t dtype, int64_t n, int32_t H, int32_t D, cons
                             static_cast<const double*>(dV), static_cast<const double*>(del),
                             static_cast<const double*>(der), static_cast<double*>(dH),
                             static_cast<double*>(da_l), static_cast<double*>(da_r), s);
+}
+
+// Projection fused with its all-gather: C = A·B written to
+// n_dst row-major M x N destinations, dst[0] local and dst[1..] the same rows
+// of the other ranks' tables through peer-mapped addresses — the TMA-store
+// epilogue sends every finished tile to all of them, so the exchange
+// overlaps the remaining tiles' MMAs instead of following the GEMM.
+extern "C" int gf_gemm_bcast(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                             const void* B, void* const* dst, int32_t n_dst, void* stream) {
+  if (!dst || n_dst < 1 || n_dst > 8 || M < 0 || N < 0 || K < 0 || M >= (1LL << 31) ||
+      N >= (1LL << 31) || K >= (1LL << 31)) {
+    gfb::set_error("gf_gemm_bcast: invalid arguments (1 <= n_dst <= 8)");
+    return GF_ERR_INVALID;
+  }
+  for (int i = 0; i < n_dst; ++i)
+    if (!dst[i] || (reinterpret_cast<uintptr_t>(dst[i]) & 15u)) {
+      gfb::set_error("gf_gemm_bcast: destinations must be non-null and 16 B aligned");
+      return GF_ERR_INVALID;
+    }
+  if (M == 0 || N == 0) return GF_OK;
+  if (!gfb::tma_gemm_eligible(dtype, 0, M, N, K, A, dst[0]) || N % 32) {
+    gfb::set_error("gf_gemm_bcast: needs fp32, K % 4 == 0, N % 32 == 0, 16 B aligned operands");
+    return GF_ERR_INVALID;
+  }
+  float* peers[8];
+  for (int i = 1; i < n_dst; ++i) peers[i - 1] = static_cast<float*>(dst[i]);
+  return gfb::tma_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
+                       static_cast<float*>(dst[0]), 0, static_cast<cudaStream_t>(stream), peers,
+                       n_dst - 1);
 }

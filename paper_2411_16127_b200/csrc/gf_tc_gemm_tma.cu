@@ -134,6 +134,15 @@ __device__ __forceinline__ float lo_of(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+// Extra destinations of the output tile (projection -> all-gather fused):
+// the same C rows in other ranks' tables, reached through peer-mapped
+// (NVLink / NVSwitch) addresses; the epilogue's TMA stores go to every one.
+constexpr int kMaxPeers = 7;
+struct PeerMaps {
+  CUtensorMap map[kMaxPeers];
+  int n;
+};
+
 struct Layout {  // byte offsets of one stage inside the dynamic smem
   uint32_t a_raw, a_lo, b_raw, b_lo, bytes;
 };
@@ -154,7 +163,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_braw,
                     const __grid_constant__ CUtensorMap map_blo,
-                    const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int nt,
+                    const __grid_constant__ CUtensorMap map_c,
+                    const __grid_constant__ PeerMaps peers, int M, int N, int K, int nt,
                     int stages, int bres, int tma_out, float* __restrict__ C, int accumulate) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024 B-align the stage area (the swizzle pattern assumes it)
@@ -306,6 +316,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           epi_bar();
           if (t == 0) {
             tma_store_2d(&map_c, n_idx * nt + c0, m * TM, buf, accumulate != 0);
+            for (int p = 0; p < peers.n; ++p)  // same tile into the peers' tables
+              tma_store_2d(&peers.map[p], n_idx * nt + c0, m * TM, buf, accumulate != 0);
             bulk_commit();
           }
         }
@@ -400,7 +412,11 @@ int env_int(const char* name, int dflt) {
 }
 
 int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
-             int accumulate, cudaStream_t s) {
+             int accumulate, cudaStream_t s, float* const* peer_c, int n_peers) {
+  if (n_peers < 0 || n_peers > kMaxPeers) {
+    set_error("gf_gemm_bcast: at most 8 destinations");
+    return GF_ERR_INVALID;
+  }
   // GF_TMA_NT / GF_TMA_BRES: A/B overrides of the tile width and B residency
   int nt = pick_nt(N);
   const int nt_env = env_int("GF_TMA_NT", 0);
@@ -413,7 +429,16 @@ int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, fl
   GF_CHECK_LAUNCH("split_b_kernel");
   CUtensorMap ma, mbr, mbl, mc;
   const bool tma_out = nt % 32 == 0 && N % 4 == 0;  // C rows 16 B aligned for the TMA store
-  if (!make_map(&ma, A, M, K, TM) || !make_map(&mbr, braw, N, K, nt) ||
+  PeerMaps pm;
+  pm.n = n_peers;
+  if (n_peers > 0 && !tma_out) {
+    cudaFreeAsync(bsplit, s);
+    set_error("gf_gemm_bcast: N must be a multiple of 32 (TMA-store epilogue)");
+    return GF_ERR_INVALID;
+  }
+  bool peer_ok = true;
+  for (int p = 0; p < n_peers; ++p) peer_ok = peer_ok && make_map(&pm.map[p], peer_c[p], M, N, TM);
+  if (!peer_ok || !make_map(&ma, A, M, K, TM) || !make_map(&mbr, braw, N, K, nt) ||
       !make_map(&mbl, blo, N, K, nt) || (tma_out && !make_map(&mc, C, M, N, TM))) {
     cudaFreeAsync(bsplit, s);
     set_error("gf_gemm: cuTensorMapEncodeTiled failed");
@@ -439,7 +464,7 @@ int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, fl
   int grid = static_cast<int>(std::min<int64_t>(m_tiles * n_tiles, 148));
   grid = std::max(n_tiles, grid / n_tiles * n_tiles);
   if (!tma_out) mc = ma;  // unused
-  tma_gemm_kernel<<<grid, NUM_THREADS, smem, s>>>(ma, mbr, mbl, mc, static_cast<int>(M),
+  tma_gemm_kernel<<<grid, NUM_THREADS, smem, s>>>(ma, mbr, mbl, mc, pm, static_cast<int>(M),
                                                   static_cast<int>(N), static_cast<int>(K), nt,
                                                   stages, bres ? 1 : 0, tma_out ? 1 : 0, C,
                                                   accumulate);

@@ -239,6 +239,21 @@ def gemm(A, B, trans_a=False, out=None, accumulate=False, stream=None):
     return out
 
 
+def gemm_bcast(A, B, outs, stream=None):
+    """C = A @ B stored tile by tile into every tensor of `outs` (gf_gemm_bcast):
+    outs[0] local, outs[1..] the same rows of peer ranks' tables (peer-mapped
+    views, e.g. torch symmetric memory buffers).  fp32, N % 32 == 0."""
+    M, K = A.shape
+    N = B.shape[1]
+    for o in outs:
+        if tuple(o.shape) != (M, N) or not o.is_contiguous():
+            raise ValueError("gemm_bcast: every destination must be a contiguous M x N view")
+    arr = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    check(lib().gf_gemm_bcast(DTYPES[A.dtype], M, N, K, _p(A), _p(B), arr, len(outs),
+                              _stream(stream)), "gf_gemm_bcast")
+    return outs[0]
+
+
 def gat_logits(Hf, a_l, a_r, heads, head_dim, stream=None, el=None, er=None):
     n = Hf.shape[0]
     el = torch.empty(n, heads, dtype=Hf.dtype, device=Hf.device) if el is None else el

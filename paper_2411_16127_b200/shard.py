@@ -125,3 +125,59 @@ def all_gather_rows(table: torch.Tensor, shard: RowShard, group=None, async_op=F
 
     blk = table[shard.block]
     return dist.all_gather_into_tensor(table, blk, group=group, async_op=async_op)
+
+
+def block_views(tables: list, shard: RowShard) -> list:
+    """Destinations of this rank's block for a producer that writes every
+    rank's copy of a padded table: [own table's block, then the same rows of
+    each peer's table in rank order].  `tables[k]` is rank k's table (a
+    peer-mapped view for k != rank)."""
+    if len(tables) != shard.world:
+        raise ValueError("block_views: one table per rank expected")
+    order = [shard.rank] + [k for k in range(shard.world) if k != shard.rank]
+    return [tables[k][shard.block] for k in order]
+
+
+class PeerTables:
+    """Padded node tables in symmetric memory (torch.distributed.
+    _symmetric_memory): every rank's copy is addressable from every GPU
+    through NVLink / NVSwitch peer mappings, so the kernel that produces a
+    rank's block writes it straight into all copies (gf_gemm_bcast: the
+    projection with its all-gather fused into the epilogue) and a device-side
+    barrier replaces the collective.  One symmetric buffer holds all tables."""
+
+    def __init__(self, shard: RowShard, widths: dict, dtype=torch.float32, device=None,
+                 group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.shard = shard
+        group = group if group is not None else dist.group.WORLD
+        n = shard.n_padded
+        total = n * sum(widths.values())
+        self.buf = symm_mem.empty(total, dtype=dtype, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        self.peer_bufs = [self.buf if k == shard.rank else
+                          self.hdl.get_buffer(k, (total,), dtype, 0) for k in range(shard.world)]
+        self.offsets = {}
+        off = 0
+        for name, w in widths.items():
+            self.offsets[name] = (off, w)
+            off += n * w
+
+    def _table(self, buf, name):
+        off, w = self.offsets[name]
+        return buf[off: off + self.shard.n_padded * w].view(self.shard.n_padded, w)
+
+    def table(self, name) -> torch.Tensor:
+        """This rank's full padded table."""
+        return self._table(self.buf, name)
+
+    def dests(self, name) -> list:
+        """gemm_bcast destinations of this rank's block (own first)."""
+        return block_views([self._table(b, name) for b in self.peer_bufs], self.shard)
+
+    def barrier(self):
+        """Device-side barrier on the current stream: every rank's writes
+        issued before it are visible to every rank after it."""
+        self.hdl.barrier(channel=0)

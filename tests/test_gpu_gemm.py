@@ -109,3 +109,42 @@ def test_gat_logits_and_fanin_fp32_fast_path(cuda, n):
     assert float(np.abs(dar.cpu().numpy() - ref_ar).max()) / scale < 1e-4
     _, dal2, _ = fused.gat_fanin(t(Hf), t(al), t(ar), t(dV), t(dl), t(dr), H, D)
     assert torch.equal(dal, dal2)
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 64, 64), (4099, 128, 128), (257, 96, 32)])
+def test_gemm_bcast_matches_gemm(cuda, M, N, K):
+    """Projection fused with the row all-gather: every destination (here local
+    row blocks of larger tables standing in for the peers' tables) receives the
+    bit-identical product."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + N)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(K, N, device="cuda", generator=g) * 2 - 1
+    ref = fused.gemm(A, B)
+    tables = [torch.full((3 * M, N), 7.0, device="cuda") for _ in range(4)]
+    outs = [t[M: 2 * M] for t in tables]
+    fused.gemm_bcast(A, B, outs)
+    torch.cuda.synchronize()
+    for t in tables:
+        assert torch.equal(t[M: 2 * M], ref)
+        assert bool((t[:M] == 7.0).all()) and bool((t[2 * M:] == 7.0).all())  # nothing else written
+    one = torch.empty(M, N, device="cuda")
+    fused.gemm_bcast(A, B, [one])
+    assert torch.equal(one, ref)
+
+
+def test_gemm_bcast_errors(cuda):
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    A = torch.rand(64, 32, device="cuda")
+    with pytest.raises(Exception, match="gemm_bcast"):
+        fused.gemm_bcast(A, torch.rand(32, 48, device="cuda"), [torch.empty(64, 48, device="cuda")])
+    with pytest.raises(Exception, match="gemm_bcast"):
+        fused.gemm_bcast(A, torch.rand(32, 64, device="cuda"),
+                         [torch.empty(64, 64, device="cuda")] * 9)

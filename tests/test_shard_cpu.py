@@ -135,3 +135,30 @@ def test_partition_balances_edges():
         assert b[0] == 0 and b[-1] == g.n and all(x <= y for x, y in zip(b, b[1:]))
         load = [int(rp[b[k + 1]] - rp[b[k]] + cp[b[k + 1]] - cp[b[k]]) for k in range(world)]
         assert max(load) - min(load) <= 2 * int(np.diff(g.row_ptr).max() + np.diff(g.csc_ptr).max())
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_block_views_write_every_copy(world):
+    """gemm_bcast addressing (shard.block_views): when every rank writes its
+    block through its destination list into all ranks' padded tables, every
+    copy equals the all-gathered table, and nothing outside the blocks moves."""
+    from paper_2411_16127_b200.shard import RowShard, block_views
+
+    g = make_graph()
+    rp, col = torch.from_numpy(g.row_ptr), torch.from_numpy(g.col)
+    cp, cr = torch.from_numpy(g.csc_ptr), torch.from_numpy(g.csc_row)
+    shards = [RowShard.build(g.n, rp, col, cp, cr, k, world) for k in range(world)]
+    x = torch.randn(g.n, 6)
+    xp = shards[0].to_padded(x)
+    tables = [torch.full_like(xp, float("nan")) for _ in range(world)]
+    for k, sh in enumerate(shards):
+        dests = block_views(tables, sh)
+        assert dests[0].data_ptr() == tables[k][sh.block].data_ptr()  # own copy first
+        assert len(dests) == world
+        for d in dests:
+            d.copy_(xp[sh.block])
+    for t in tables:
+        assert torch.equal(t, xp)
+        assert torch.equal(shards[0].from_padded(t), x)
+    with pytest.raises(ValueError):
+        block_views(tables[:-1] if world > 1 else [], shards[0])

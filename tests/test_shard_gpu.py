@@ -61,3 +61,41 @@ def test_sharded_equals_single_gpu(cuda, world, cfg):
     torch.cuda.synchronize()
     for a, b, name in ((O1, Op, "O"), (dQ1, dQp, "dQ"), (dK1, dKp, "dK"), (dV1, dVp, "dV")):
         assert torch.equal(a, s0.from_padded(b)), name
+
+
+def test_peer_tables_gemm_bcast_world1(cuda):
+    """The p2p exchange plumbing on one GPU: a 1-rank NCCL group, padded tables
+    in torch symmetric memory, gemm_bcast into shard.PeerTables.dests, device
+    barrier.  (With more ranks the destinations add the peers' tables; the
+    addressing is covered on CPU by test_shard_cpu.test_block_views_*.)"""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2411_16127_b200 import fused
+    from paper_2411_16127_b200.shard import PeerTables, RowShard
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = graph(n=500)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)  # noqa: E731
+        sh = RowShard.build(g.n, t(g.row_ptr), t(g.col), t(g.csc_ptr), t(g.csc_row), 0, 1)
+        pt = PeerTables(sh, {"Q": 64, "V": 128}, device=cuda)
+        X = torch.rand(sh.n_padded, 32, device=cuda)
+        Wq, Wv = torch.rand(32, 64, device=cuda), torch.rand(32, 128, device=cuda)
+        pt.barrier()
+        fused.gemm_bcast(X[sh.block], Wq, pt.dests("Q"))
+        fused.gemm_bcast(X[sh.block], Wv, pt.dests("V"))
+        pt.barrier()
+        torch.cuda.synchronize()
+        assert torch.equal(pt.table("Q"), fused.gemm(X, Wq))
+        assert torch.equal(pt.table("V"), fused.gemm(X, Wv))
+    finally:
+        dist.destroy_process_group()
