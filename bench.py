@@ -694,6 +694,57 @@ def e2e_pipelined(dg, spec, tabs, stream, steps, warmup=2):
     return start.elapsed_time(end) / steps
 
 
+def e2e_graphed(dg, spec, tabs, hin, hout, flush, steps):
+    """The serial end-to-end step (H2D of Q|el, K|er, V, dO from pinned host
+    memory -> forward -> pass A -> pass B -> D2H of O, dQ|del, dK|der, dV)
+    captured once into a CUDA graph and replayed: one launch per step instead
+    of eleven API calls, which is what bounds the small graphs (C1-C3).
+    L2 flushed between replays.  Returns {"ms": ...} or {"error": ...}."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    Q, K, V, dO = (tabs[k] for k in ("Q", "K", "V", "dO"))
+    O, st, dQ, dK, dV = (tabs[k] for k in ("O", "stats", "dQ", "dK", "dV"))
+
+    def body():
+        cs = torch.cuda.current_stream()
+        for h, d in zip(hin, (Q, K, V, dO)):
+            d.copy_(h, non_blocking=True)
+        fused.attn_forward(dg, spec, Q, K, V, O=O, stats=st, stream=cs)
+        fused.attn_backward_rows(dg, spec, Q, K, V, O, st, dO, dK, stream=cs)
+        fused.attn_backward_cols(dg, spec, Q, K, V, st, dO, dQ, dV, stream=cs)
+        for h, d in zip(hout, (O, dQ, dK, dV)):
+            h.copy_(d, non_blocking=True)
+
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            body()  # warm-up outside the capture
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        del g
+        return {"ms": statistics.mean(ts)}
+    except Exception as ex:  # reported, the other e2e numbers stand
+        torch.cuda.synchronize()
+        return {"error": f"{type(ex).__name__}: {str(ex)[:160]}"}
+
+
 def run_ours(args, rank, world):
     import numpy as np
     import torch
@@ -826,7 +877,7 @@ def run_ours(args, rank, world):
     value = e * args.steps / (sum_ms / 1e3) / 1e9
 
     # ---- e2e through the C-ABI with pinned host buffers
-    e2e_val, e2e_serial, h2d, d2h = None, None, 0, 0
+    e2e_val, e2e_serial, h2d, d2h, e2e_graph = None, None, 0, 0, None
     if not sharded:
         hQ, hK, hV, hdO = [x.cpu().pin_memory() for x in (Q, K, V, dO)]
         hO, hdQ, hdK, hdV = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (O, dQ, dK, dV)]
@@ -885,6 +936,10 @@ def run_ours(args, rank, world):
                 "dV": dV}
         e2e_ms = e2e_pipelined(dg, spec, tabs, stream, args.steps)
         e2e_val = e / (e2e_ms / 1e3) / 1e9
+        e2e_graph = e2e_graphed(dg, spec, tabs, (hQ, hK, hV, hdO), (hO, hdQ, hdK, hdV), flush,
+                                max(3, args.steps // 2))
+        if e2e_graph.get("ms"):
+            e2e_graph["value"] = e / (e2e_graph["ms"] / 1e3) / 1e9
     else:
         # Row-sharded: every rank uploads ITS OWN rows of Q|el, K|er, V, dO from
         # pinned host memory, runs the step (NCCL all-gathers included) and
@@ -1028,6 +1083,11 @@ def run_ours(args, rank, world):
                              "rows of the inputs and downloads its own rows of the outputs every "
                              "step, NCCL all-gathers inside the step; max over ranks"),
                     "serial_value": e2e_serial,
+                    "graph_value": (e2e_graph or {}).get("value"),
+                    "graph_mode": "the serial step (copies + 3 kernels) captured in one CUDA "
+                                  "graph and replayed, L2 flushed between replays"
+                                  + (f"; capture failed: {e2e_graph['error']}"
+                                     if e2e_graph and "error" in e2e_graph else ""),
                     "serial_mode": "one step at a time (copies overlap only within the step), "
                                    "L2 flushed between steps"},
             "layer": layer_out,
