@@ -227,6 +227,17 @@ int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const void* Q, cons
  * Row-major, fp32 or fp64; accumulate = 1 adds into C. */
 int gf_gemm(int32_t dtype, int32_t trans_a, int64_t M, int64_t N, int64_t K, const void* A,
             const void* B, void* C, int32_t accumulate, void* stream);
+/* Merge of source-phased forward partials (row-sharded overlap, SURVEY
+ * §8(e)): part k is the forward over the in-edges whose sources lie in block
+ * k (its sub-graph row pointer row_ptrs[k], normalised O_parts[k] rows x F,
+ * records rec_parts[k] rows x H x 4).  Per (row, head): m = max m_k,
+ * w_k = l_k e^(m_k - m), O = sum w_k O_k / sum w_k, record {m, log2 sum w_k,
+ * aux}; delta untouched; parts empty in a row are skipped, rows empty in all
+ * parts untouched.  1 <= parts <= 8, heads <= 32.  All arrays row-relative. */
+int gf_attn_merge_parts(int32_t dtype, int64_t rows, int32_t heads, int32_t head_dim,
+                        int32_t parts, const int32_t* const* row_ptrs, const void* const* O_parts,
+                        const void* const* rec_parts, void* O, void* rec, void* stream);
+
 /* Projection fused with its all-gather: C = A·B (fp32,
  * 3xTF32 tcgen05, A M x K, B K x N row-major) stored by the TMA epilogue to
  * n_dst (1..8) row-major M x N destinations — dst[0] local, dst[1..] the

@@ -91,6 +91,9 @@ SIGNATURES = {
                                    _vp]),
     "gf_attn_bwd_cols": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp]),
+    "gf_attn_merge_parts": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_void_p), _vp, _vp, _vp]),
     "gf_gemm_bcast": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp,
                                 C.POINTER(C.c_void_p), C.c_int32, _vp]),
     "gf_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp,

@@ -239,6 +239,22 @@ def gemm(A, B, trans_a=False, out=None, accumulate=False, stream=None):
     return out
 
 
+def attn_merge_parts(spec: AttnSpec, row_ptrs, O_parts, rec_parts, O, stats, stream=None):
+    """Combine source-phased forward partials (gf_attn_merge_parts): part k =
+    the forward over the in-edges from source block k (row pointer row_ptrs[k],
+    normalised O_parts[k], records rec_parts[k]); all row-relative views of the
+    same rows.  Writes O and the records' {m, log2 l, aux}."""
+    n = len(O_parts)
+    if not (len(row_ptrs) == len(rec_parts) == n):
+        raise ValueError("attn_merge_parts: one row pointer, O and record table per part")
+    rows = O.shape[0]
+    arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() for t in ts])  # noqa: E731
+    check(lib().gf_attn_merge_parts(DTYPES[O.dtype], rows, spec.heads, spec.head_dim, n,
+                                    arr(row_ptrs), arr(O_parts), arr(rec_parts), _p(O), _p(stats),
+                                    _stream(stream)), "gf_attn_merge_parts")
+    return O, stats
+
+
 def gemm_bcast(A, B, outs, stream=None):
     """C = A @ B stored tile by tile into every tensor of `outs` (gf_gemm_bcast):
     outs[0] local, outs[1..] the same rows of peer ranks' tables (peer-mapped

@@ -181,3 +181,93 @@ class PeerTables:
         """Device-side barrier on the current stream: every rank's writes
         issued before it are visible to every rank after it."""
         self.hdl.barrier(channel=0)
+
+
+# ------------------------------------------------- source-phased forward --
+# The forward gathers source rows of every rank, so its all-gather cannot
+# simply run under it.  But CSR rows are sorted by source and every rank's
+# sources are one contiguous id block, so each row's in-edges split into P
+# contiguous slices by source block.  Running the forward once per block — the
+# local block first, then each block as its rows arrive — and merging the
+# normalised partials (gf_attn_merge_parts) overlaps the exchange with the
+# forward ("chunked all-gather overlapped with compute on locally-sourced
+# edges first", SURVEY §8(e)).  Deterministic; equal to the one-pass forward
+# up to the merge's rounding (the one-pass path stays bitwise equal to 1 GPU).
+
+@dataclass
+class SourceParts:
+    shard: RowShard
+    graphs: list    # DeviceGraph of the rank's rows restricted to source block k
+    row_ptrs: list  # int32 [n_padded + 1] row pointer of each part (device)
+
+
+def source_parts(shard: RowShard, cta_threshold: int = 0, stream=None) -> SourceParts:
+    from .fused import DeviceGraph
+
+    R, P, n = shard.R, shard.world, shard.n_padded
+    rp = shard.row_ptr.to(torch.int64)
+    col = shard.col.to(torch.int64)
+    dev = col.device
+    deg = rp[1:] - rp[:-1]
+    row_of = torch.repeat_interleave(torch.arange(n, device=dev), deg)
+    blk = col // R
+    counts = torch.zeros(n * P, dtype=torch.int64, device=dev)
+    counts.index_add_(0, row_of * P + blk, torch.ones_like(blk))
+    counts = counts.view(n, P)
+    empty_ptr = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+    dummy = torch.zeros(1, dtype=torch.int32, device=dev)
+    graphs, ptrs = [], []
+    for k in range(P):
+        ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        ptr[1:] = torch.cumsum(counts[:, k], 0)
+        ck = col[blk == k].to(torch.int32)
+        ptr = ptr.to(torch.int32)
+        ptrs.append(ptr)
+        graphs.append(DeviceGraph.from_split(n, ptr, ck if ck.numel() else dummy, empty_ptr,
+                                             dummy, cta_threshold=cta_threshold, skip_empty=True,
+                                             stream=stream))
+    return SourceParts(shard, graphs, ptrs)
+
+
+def part_buffers(parts: SourceParts, spec, dtype=torch.float32, device=None):
+    """Row-block-sized partial outputs: one R x F O and R x H x 4 record table
+    per part (the kernels address them in the padded id space through a base
+    pointer offset by the rank's first row)."""
+    R = parts.shard.R
+    O = [torch.empty(R, spec.F, dtype=dtype, device=device) for _ in parts.graphs]
+    rec = [torch.empty(R, spec.heads, 4, dtype=dtype, device=device) for _ in parts.graphs]
+    return O, rec
+
+
+def phase_forward(parts: SourceParts, k: int, spec, Q, K, V, O_parts, rec_parts, stream=None):
+    """Forward over source block k's in-edges of the rank's rows into part k."""
+    import ctypes as C
+
+    from ._capi import check, lib
+    from .fused import _stream
+
+    sh = parts.shard
+    es = V.element_size()
+    row0 = sh.rank * sh.R
+    o_base = O_parts[k].data_ptr() - row0 * spec.F * es
+    r_base = rec_parts[k].data_ptr() - row0 * spec.heads * 4 * es
+    d = spec.desc(V.dtype)
+    check(lib().gf_attn_fwd(parts.graphs[k].handle, C.byref(d), C.c_void_p(Q.data_ptr()),
+                            C.c_void_p(K.data_ptr()), C.c_void_p(V.data_ptr()),
+                            C.c_void_p(o_base), C.c_void_p(r_base), None, _stream(stream)),
+          "gf_attn_fwd (phase)")
+
+
+def merge_phases(parts: SourceParts, spec, O_parts, rec_parts, O, stats, stream=None):
+    """O / records of the rank's block from the per-block partials."""
+    from .fused import attn_merge_parts
+
+    sh = parts.shard
+    blk = sh.block
+    ptrs = [p[blk.start: blk.stop + 1] for p in parts.row_ptrs]
+    attn_merge_parts(spec, ptrs, O_parts, rec_parts, O[blk], stats[blk], stream=stream)
+
+
+def phase_order(shard: RowShard) -> list:
+    """Own block first (its rows are local), then the others in rank order."""
+    return [shard.rank] + [k for k in range(shard.world) if k != shard.rank]
