@@ -311,6 +311,8 @@ def main():
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
                     help="sharded training step: projected rows exchanged by the projection's own "
                          "epilogue into symmetric memory (p2p) or by NCCL all-gather")
+    ap.add_argument("--phased", choices=("auto", "on", "off"), default="auto",
+                    help="sharded step: source-phased forward overlapping the source-row exchange")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args()
@@ -812,13 +814,47 @@ def run_ours(args, rank, world):
     dQ, dK, dV = (torch.zeros(n_tab, qk, device=dev), torch.zeros(n_tab, qk, device=dev),
                   torch.zeros(n_tab, F, device=dev))
     NEV = 6 if sharded else 4
+    # Source-phased forward (shard.py): the source rows arrive per block
+    # (broadcast from each owner) while the forward runs block by block, own
+    # block first, then the partials are merged.  "auto": when the modelled
+    # exposed exchange (the V, Q|el blocks of the other ranks at ~700 GB/s)
+    # exceeds twice the phases' extra cost (partial O / records written and
+    # merged, one launch per block).
+    phased = False
+    if sharded:
+        from paper_2411_16127_b200 import shard as shard_mod
+
+        row_b = 4 * (F + qk)
+        ag_ms = (world - 1) / world * n_tab * row_b / 700e9 * 1e3
+        # partials written, read back and merged (measured at N = 1: C5 GT +1.1 ms)
+        extra_ms = world * shard.R * (F + 4 * H) * 4 * 3 / 5e12 * 1e3 + world * 0.02
+        phased = args.phased == "on" or (args.phased == "auto" and ag_ms > 2 * extra_ms)
+        if phased:
+            parts = shard_mod.source_parts(shard, cta_threshold=args.cta_threshold)
+            O_parts, rec_parts = shard_mod.part_buffers(parts, spec, device=dev)
+            order = shard_mod.phase_order(shard)
 
     def step(ev=None):
         rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
         k = 0
         rec(k)
         later = []
-        if sharded:
+        if sharded and phased:
+            R = shard.R
+            blocks = {b: [torch.distributed.broadcast(t[b * R:(b + 1) * R], src=b, async_op=True)
+                          for t in (V, Q)] for b in range(world)}
+            later = [all_gather_rows(t, shard, async_op=True)
+                     for t in (dO,) + ((K,) if layer != "gat" else ())]
+            k += 1
+            rec(k)
+            for b in order:  # own block first: its rows are already local
+                if b != rank:
+                    for w in blocks[b]:
+                        w.wait()
+                shard_mod.phase_forward(parts, b, spec, Q, K, V, O_parts, rec_parts,
+                                        stream=stream)
+            shard_mod.merge_phases(parts, spec, O_parts, rec_parts, O, stats, stream=stream)
+        elif sharded:
             # exchange 1: source-side rows the forward gathers (V, Q|el) — waited
             # on; then dO and, for dot models, K (only pass B gathers them) are
             # issued on NCCL's stream and overlap the forward and pass A
@@ -829,7 +865,8 @@ def run_ours(args, rank, world):
                 w.wait()
             k += 1
             rec(k)
-        fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream)
+        if not phased:
+            fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream)
         k += 1
         rec(k)
         fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK, stream=stream)
@@ -1044,6 +1081,7 @@ def run_ours(args, rank, world):
                                        "(graph.cpp:25-78), then degree stats, buckets and "
                                        "schedules; the reference's CPU from_coo is 16.9 s on C4 "
                                        "(SURVEY a2)"} if not sharded else None),
+            "phased_forward": phased if sharded else None,
             "allgather_ms": ({"src_rows_exposed": round(statistics.mean(k_ag1), 4),
                               "dO_K_records_exposed": round(statistics.mean(k_ag2), 4),
                               "note": "exposed on the compute stream: dO (and K for dot "
