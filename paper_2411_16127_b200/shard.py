@@ -201,9 +201,10 @@ class SourceParts:
     row_ptrs: list  # int32 [n_padded + 1] row pointer of each part (device)
 
 
-def source_parts(shard: RowShard, cta_threshold: int = 0, stream=None) -> SourceParts:
-    from .fused import DeviceGraph
-
+def source_split(shard: RowShard) -> list:
+    """[(row_ptr_k, col_k)] per source block k: the rank's CSR restricted to
+    in-edges whose (padded) source id lies in [k R, (k+1) R), rows and each
+    row's sources in their original order (int32, on the shard's device)."""
     R, P, n = shard.R, shard.world, shard.n_padded
     rp = shard.row_ptr.to(torch.int64)
     col = shard.col.to(torch.int64)
@@ -214,14 +215,23 @@ def source_parts(shard: RowShard, cta_threshold: int = 0, stream=None) -> Source
     counts = torch.zeros(n * P, dtype=torch.int64, device=dev)
     counts.index_add_(0, row_of * P + blk, torch.ones_like(blk))
     counts = counts.view(n, P)
-    empty_ptr = torch.zeros(n + 1, dtype=torch.int32, device=dev)
-    dummy = torch.zeros(1, dtype=torch.int32, device=dev)
-    graphs, ptrs = [], []
+    out = []
     for k in range(P):
         ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         ptr[1:] = torch.cumsum(counts[:, k], 0)
-        ck = col[blk == k].to(torch.int32)
-        ptr = ptr.to(torch.int32)
+        out.append((ptr.to(torch.int32), col[blk == k].to(torch.int32)))
+    return out
+
+
+def source_parts(shard: RowShard, cta_threshold: int = 0, stream=None) -> SourceParts:
+    from .fused import DeviceGraph
+
+    n = shard.n_padded
+    dev = shard.col.device
+    empty_ptr = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+    dummy = torch.zeros(1, dtype=torch.int32, device=dev)
+    graphs, ptrs = [], []
+    for ptr, ck in source_split(shard):
         ptrs.append(ptr)
         graphs.append(DeviceGraph.from_split(n, ptr, ck if ck.numel() else dummy, empty_ptr,
                                              dummy, cta_threshold=cta_threshold, skip_empty=True,

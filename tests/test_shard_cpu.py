@@ -94,6 +94,16 @@ def worker(rank, world, port, errq):
         for w in works:
             w.wait()
         assert all(torch.equal(m, x) for m, x in zip(mines, tabs))
+        # (3c) the phased step's exchange: one async broadcast per owner block
+        # (every rank issues them in the same order), waited on own block first
+        R = sh.R
+        bmine = torch.zeros_like(full)
+        bmine[sh.block] = full[sh.block]
+        bw = {k: dist.broadcast(bmine[k * R:(k + 1) * R], src=k, async_op=True)
+              for k in range(world)}
+        for k in [rank] + [j for j in range(world) if j != rank]:
+            bw[k].wait()
+        assert torch.equal(bmine, full)
         # (4) sharded forward == single-process forward on owned rows, bitwise
         csr = oracle.CSR(sh.n_padded, rp, col, cp, cr, np.zeros(len(cr), np.int64))
         Op = oracle.forward(csr, sh.to_padded(t(Q)).numpy(), sh.to_padded(t(K)).numpy(),
@@ -162,3 +172,52 @@ def test_block_views_write_every_copy(world):
         assert torch.equal(shards[0].from_padded(t), x)
     with pytest.raises(ValueError):
         block_views(tables[:-1] if world > 1 else [], shards[0])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_source_split_and_merge_cpu(world):
+    """shard.source_split partitions every owned row's in-edges by source block
+    (order kept), and the forward over the parts merged with the
+    gf_attn_merge_parts rule (m = max m_k, w_k = l_k e^(m_k - m)) equals the
+    one-pass forward (CPU oracle)."""
+    import oracle
+    from paper_2411_16127_b200.shard import RowShard, source_split
+
+    g = make_graph(seed=4)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    rng = np.random.default_rng(5)
+    H, D = 2, 8
+    Q, K, V = (rng.uniform(-1, 1, (g.n, H * D)) for _ in range(3))
+    O_ref = oracle.forward(g, Q, K, V, H, D, "dot", False, 0.4, 0.2)
+    for rank in range(world):
+        sh = RowShard.build(g.n, t(g.row_ptr), t(g.col), t(g.csc_ptr), t(g.csc_row), rank, world)
+        Qp, Kp, Vp = (sh.to_padded(t(x)).numpy() for x in (Q, K, V))
+        rp, col = sh.row_ptr.numpy().astype(np.int64), sh.col.numpy().astype(np.int64)
+        parts = source_split(sh)
+        assert sum(int(c.numel()) for _, c in parts) == len(col)
+        for v in range(sh.n_padded):
+            joined = np.concatenate([c.numpy()[p[v]: p[v + 1]] for p, c in parts])
+            assert np.array_equal(joined, col[rp[v]: rp[v + 1]])  # blocks in order = the row
+        # merge with the lse form of the rule: w_k = e^(lse_k - max_k lse_k)
+        num = np.zeros((sh.n_padded, H * D))
+        outs = []
+        for p, c in parts:
+            p64, c64 = p.numpy().astype(np.int64), c.numpy().astype(np.int64)
+            csr = oracle.CSR(sh.n_padded, p64, c64, np.zeros(sh.n_padded + 1, np.int64),
+                             np.zeros(0, np.int64), np.zeros(0, np.int64))
+            Ok, lse = oracle.forward(csr, Qp, Kp, Vp, H, D, "dot", False, 0.4, 0.2, want_lse=True)
+            outs.append((np.diff(p64) > 0, Ok, lse))
+        top = np.full((sh.n_padded, H), -np.inf)
+        for live, _, lse in outs:
+            top = np.where(live[:, None], np.maximum(top, lse), top)
+        L = np.zeros((sh.n_padded, H))
+        for live, Ok, lse in outs:
+            with np.errstate(invalid="ignore"):  # rows with no live part: masked below
+                d = np.where(live[:, None], lse - top, 0.0)
+            w = np.where(live[:, None], np.exp(d), 0.0)
+            L += w
+            num += np.repeat(w, D, axis=1) * Ok
+        rows = sh.rows
+        got = num[rows] / np.maximum(np.repeat(L[rows], D, axis=1), 1e-300)
+        nz = np.diff(g.row_ptr)[sh.lo: sh.hi] > 0
+        assert np.allclose(got[nz], O_ref[sh.lo: sh.hi][nz], rtol=1e-12, atol=1e-12)
