@@ -119,7 +119,10 @@ def lib():
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                 "g.build()'` (no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
+        ab_build = bool(os.environ.get("GF_CUDA_LIB"))  # A/B builds may predate newer entry points
         for name, (res, args) in SIGNATURES.items():
+            if ab_build and not hasattr(L, name):
+                continue
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -120,6 +120,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const T* __restrict__ Vb = a.V + off;
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;
+  const uint32_t fb = a.F * sizeof(T), qb = qs * sizeof(T);  // row strides in bytes
 
   T dov[NE], kv[NE];
   T delta;
@@ -174,13 +175,13 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
         const int uu = ok[t] ? u : 0;
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-          ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+          ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
         if constexpr (VAR == GF_DOT) {
 #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+            ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
         } else {
-          el[t] = ld_node(Qb + uu * qs);
+          el[t] = ld_node(row_at(Qb, uu, qb));
         }
       }
 #pragma unroll
@@ -289,6 +290,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   const int off = h * a.D + (c % a.LPH) * NE;
   const size_t urow = static_cast<size_t>(u) * a.F + off;
   const T* __restrict__ dOb = a.dO + off;
+  const uint32_t fb = a.F * sizeof(T);
   const T* __restrict__ Kb = a.K + off;
   const T* __restrict__ Rb = a.stats + 4 * h;
 
@@ -337,11 +339,11 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
         const int vv = ok[t] ? v : 0;
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-          ld_gather<T, CB>(dOb + vv * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
+          ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
         if constexpr (VAR == GF_DOT) {
 #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(Kb + vv * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
+            ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
         }
         rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
       }

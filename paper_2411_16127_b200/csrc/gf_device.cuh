@@ -87,6 +87,23 @@ __device__ __forceinline__ T ld_node(const T* __restrict__ p) {
 #endif
 }
 
+// Row r of a node table with a row stride of `stride_bytes`: one
+// IMAD.WIDE.U32 (base + r * stride as a 64-bit product) instead of a signed
+// 32-bit multiply, sign extension and a scaled 64-bit add.  Valid for
+// r >= 0 (ids, and the 0 dummy row of masked lanes).
+#ifndef GF_WIDE_ADDR
+#define GF_WIDE_ADDR 1
+#endif
+template <typename T>
+__device__ __forceinline__ const T* row_at(const T* __restrict__ base, int r, uint32_t stride_bytes) {
+#if GF_WIDE_ADDR
+  return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) +
+                                    static_cast<uint64_t>(static_cast<uint32_t>(r)) * stride_bytes);
+#else
+  return base + r * static_cast<int>(stride_bytes / sizeof(T));
+#endif
+}
+
 template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
   if constexpr (CB == 32 && sizeof(T) == 4) {
