@@ -23,8 +23,14 @@
 // / softmax work is done once per edge, not once per 16 B chunk; 32/LPE edges
 // per warp step, unrolled U deep.  Nothing of size E x H is written: outputs
 // are O (N x F) and the per-(row, head) softmax records (gf_device.cuh Rec).
+#include <type_traits>
+
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
+
+#ifndef GF_FULL_CHUNK
+#define GF_FULL_CHUNK 1
+#endif
 
 namespace gfb {
 
@@ -124,77 +130,165 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       nxt = nb < ee ? (nb + lane < ee ? ld_idx(a.idx + nb + lane) : 0)
                     : (rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0);
     }
-#pragma unroll 1
-    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
-      bool ok[U];
-      T vv[U][NE], qv[U][NE], s[U];
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * ep + js;
-        ok[t] = j < cnt;
-        const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-        const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
-#pragma unroll
-        for (int k = 0; k < CPL; ++k)
-          ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
-        if constexpr (MODE == 3) {
-          s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
-        } else if constexpr (MODE != 0) {
-          s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(base + j) * a.H) : T(0);
-        } else if constexpr (VAR == GF_DOT) {
-#pragma unroll
-          for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
-        } else {
-          s[t] = ld_node(Qb + uu * qs);
-        }
-      }
-      if constexpr (MODE >= 2) {
-#pragma unroll
+#if GF_FULL_CHUNK
+    // Whole 32-edge chunks (all but a row's last) run a mask-free copy of the
+    // loop: no per-slot bounds compare / select on the ids and probabilities.
+    auto chunk = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T vv[U][NE], qv[U][NE], s[U];
+  #pragma unroll
         for (int t = 0; t < U; ++t) {
-#pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
-        }
-        continue;
-      }
-      T smax = ninf<T>();
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        if constexpr (MODE == 1) {
-          // score read from ES
-        } else if constexpr (VAR == GF_DOT) {
-          T d = T(0), qq = T(0);
-#pragma unroll
-          for (int i = 0; i < NE; ++i) {
-            d += qv[t][i] * kv[i];
-            qq += qv[t][i] * qv[t][i];
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
+          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+  #pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+          if constexpr (MODE == 3) {
+            s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
+          } else if constexpr (MODE != 0) {
+            s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(base + j) * a.H) : T(0);
+          } else if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else {
+            s[t] = ld_node(Qb + uu * qs);
           }
-          d = head_sum(d, a.LPH);
-          if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
-          s[t] = a.scale * d;
-        } else {
-          s[t] = lrelu(s[t] + erv, a.slope);
         }
-        s[t] = ok[t] ? s[t] : ninf<T>();
-        smax = s[t] > smax ? s[t] : smax;
+        if constexpr (MODE >= 2) {
+  #pragma unroll
+          for (int t = 0; t < U; ++t) {
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
+          }
+          continue;
+        }
+        T smax = ninf<T>();
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          if constexpr (MODE == 1) {
+            // score read from ES
+          } else if constexpr (VAR == GF_DOT) {
+            T d = T(0), qq = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) {
+              d += qv[t][i] * kv[i];
+              qq += qv[t][i] * qv[t][i];
+            }
+            d = head_sum(d, a.LPH);
+            if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
+            s[t] = a.scale * d;
+          } else {
+            s[t] = lrelu(s[t] + erv, a.slope);
+          }
+          s[t] = ok[t] ? s[t] : ninf<T>();
+          smax = s[t] > smax ? s[t] : smax;
+        }
+        // Lazy rescale, warp-uniform: only when some lane's running max moves.
+        if (__any_sync(kFull, smax > m)) {
+          const T mn = smax > m ? smax : m;
+          const T corr = m == mn ? T(1) : expd(m - mn);
+          l *= corr;
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] *= corr;
+          m = mn;
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const T p = ok[t] ? expd(s[t] - m) : T(0);
+          l += p;
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
+        }
       }
-      // Lazy rescale, warp-uniform: only when some lane's running max moves.
-      if (__any_sync(kFull, smax > m)) {
-        const T mn = smax > m ? smax : m;
-        const T corr = m == mn ? T(1) : expd(m - mn);
-        l *= corr;
-#pragma unroll
-        for (int i = 0; i < NE; ++i) acc[i] *= corr;
-        m = mn;
-      }
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const T p = ok[t] ? expd(s[t] - m) : T(0);
-        l += p;
-#pragma unroll
-        for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
+    };
+    // (only when the loop's slots tile the chunk exactly — EPW * U divides 32 —
+    // and for one-chunk lanes: the CPL = 2 shapes (GT 8x16) measured slower)
+    if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
+      chunk(std::true_type{});
+    else
+      chunk(std::false_type{});
+#else
+    {
+      constexpr bool FULL = false;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T vv[U][NE], qv[U][NE], s[U];
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
+          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+  #pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+          if constexpr (MODE == 3) {
+            s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
+          } else if constexpr (MODE != 0) {
+            s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(base + j) * a.H) : T(0);
+          } else if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else {
+            s[t] = ld_node(Qb + uu * qs);
+          }
+        }
+        if constexpr (MODE >= 2) {
+  #pragma unroll
+          for (int t = 0; t < U; ++t) {
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
+          }
+          continue;
+        }
+        T smax = ninf<T>();
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          if constexpr (MODE == 1) {
+            // score read from ES
+          } else if constexpr (VAR == GF_DOT) {
+            T d = T(0), qq = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) {
+              d += qv[t][i] * kv[i];
+              qq += qv[t][i] * qv[t][i];
+            }
+            d = head_sum(d, a.LPH);
+            if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
+            s[t] = a.scale * d;
+          } else {
+            s[t] = lrelu(s[t] + erv, a.slope);
+          }
+          s[t] = ok[t] ? s[t] : ninf<T>();
+          smax = s[t] > smax ? s[t] : smax;
+        }
+        // Lazy rescale, warp-uniform: only when some lane's running max moves.
+        if (__any_sync(kFull, smax > m)) {
+          const T mn = smax > m ? smax : m;
+          const T corr = m == mn ? T(1) : expd(m - mn);
+          l *= corr;
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] *= corr;
+          m = mn;
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const T p = ok[t] ? expd(s[t] - m) : T(0);
+          l += p;
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
+        }
       }
     }
+#endif
     if (pk) break;
   }
   if (!pk && eb >= ee) nxt = rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0;
