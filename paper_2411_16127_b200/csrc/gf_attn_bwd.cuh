@@ -24,8 +24,17 @@
 //                          add: del[u] += dS lrelu'(pre)
 // AGNN's L2 Jacobian is applied in each pass's epilogue on the owned row.
 // Scheduling and lane mapping mirror the forward (gf_attn_fwd.cuh).
+#include <type_traits>
+
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
+
+#ifndef GF_FULL_CHUNK_A
+#define GF_FULL_CHUNK_A 1
+#endif
+#ifndef GF_FULL_CHUNK_B
+#define GF_FULL_CHUNK_B 1
+#endif
 
 namespace gfb {
 
@@ -163,62 +172,132 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
       nxt = nb < ee ? (nb + lane < ee ? ld_idx(a.idx + nb + lane) : 0)
                     : (rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0);
     }
-#pragma unroll 1
-    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
-      bool ok[U];
-      T vv[U][NE], qv[U][NE], el[U];
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * ep + js;
-        ok[t] = j < cnt;
-        const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-        const int uu = ok[t] ? u : 0;
-#pragma unroll
-        for (int k = 0; k < CPL; ++k)
-          ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
-        if constexpr (VAR == GF_DOT) {
-#pragma unroll
+#if GF_FULL_CHUNK_A
+    // whole 32-edge chunks: mask-free copy of the edge loop (as the forward)
+    auto chunk = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T vv[U][NE], qv[U][NE], el[U];
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;
+          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int uu = ok[t] ? u : 0;
+  #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
-        } else {
-          el[t] = ld_node(row_at(Qb, uu, qb));
+            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+          if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else {
+            el[t] = ld_node(row_at(Qb, uu, qb));
+          }
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          T dp = T(0);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) dp += dov[i] * vv[t][i];
+          dp = head_sum(dp, a.LPH);
+          T s, rq = T(1), pre = T(0);
+          if constexpr (VAR == GF_DOT) {
+            T d = T(0), qq = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) {
+              d += qv[t][i] * kv[i];
+              qq += qv[t][i] * qv[t][i];
+            }
+            d = head_sum(d, a.LPH);
+            if (a.l2) {
+              rq = inv_norm(head_sum(qq, a.LPH));
+              d *= rq * rk;
+            }
+            s = a.scale * d;
+          } else {
+            pre = el[t] + erv;
+            s = lrelu(pre, a.slope);
+          }
+          const T p = ok[t] ? ex2((s - mrow) * l2e<T>() - ll2) : T(0);
+          const T ds = p * (dp - delta);
+          if constexpr (VAR == GF_DOT) {
+            const T w = a.scale * ds * rq;
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) acc[i] += w * qv[t][i];
+          } else {
+            acc[0] += ds * lrelu_grad(pre, a.slope);
+          }
         }
       }
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        T dp = T(0);
-#pragma unroll
-        for (int i = 0; i < NE; ++i) dp += dov[i] * vv[t][i];
-        dp = head_sum(dp, a.LPH);
-        T s, rq = T(1), pre = T(0);
-        if constexpr (VAR == GF_DOT) {
-          T d = T(0), qq = T(0);
-#pragma unroll
-          for (int i = 0; i < NE; ++i) {
-            d += qv[t][i] * kv[i];
-            qq += qv[t][i] * qv[t][i];
+    };
+    if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
+      chunk(std::true_type{});
+    else
+      chunk(std::false_type{});
+#else
+    {
+      constexpr bool FULL = false;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T vv[U][NE], qv[U][NE], el[U];
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;
+          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int uu = ok[t] ? u : 0;
+  #pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+          if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else {
+            el[t] = ld_node(row_at(Qb, uu, qb));
           }
-          d = head_sum(d, a.LPH);
-          if (a.l2) {
-            rq = inv_norm(head_sum(qq, a.LPH));
-            d *= rq * rk;
-          }
-          s = a.scale * d;
-        } else {
-          pre = el[t] + erv;
-          s = lrelu(pre, a.slope);
         }
-        const T p = ok[t] ? ex2((s - mrow) * l2e<T>() - ll2) : T(0);
-        const T ds = p * (dp - delta);
-        if constexpr (VAR == GF_DOT) {
-          const T w = a.scale * ds * rq;
-#pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] += w * qv[t][i];
-        } else {
-          acc[0] += ds * lrelu_grad(pre, a.slope);
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          T dp = T(0);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) dp += dov[i] * vv[t][i];
+          dp = head_sum(dp, a.LPH);
+          T s, rq = T(1), pre = T(0);
+          if constexpr (VAR == GF_DOT) {
+            T d = T(0), qq = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) {
+              d += qv[t][i] * kv[i];
+              qq += qv[t][i] * qv[t][i];
+            }
+            d = head_sum(d, a.LPH);
+            if (a.l2) {
+              rq = inv_norm(head_sum(qq, a.LPH));
+              d *= rq * rk;
+            }
+            s = a.scale * d;
+          } else {
+            pre = el[t] + erv;
+            s = lrelu(pre, a.slope);
+          }
+          const T p = ok[t] ? ex2((s - mrow) * l2e<T>() - ll2) : T(0);
+          const T ds = p * (dp - delta);
+          if constexpr (VAR == GF_DOT) {
+            const T w = a.scale * ds * rq;
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) acc[i] += w * qv[t][i];
+          } else {
+            acc[0] += ds * lrelu_grad(pre, a.slope);
+          }
         }
       }
     }
+#endif
     if (pk) break;
   }
   if (!pk && eb >= ee) nxt = rsn.y + lane < rsn.z ? ld_idx(a.idx + rsn.y + lane) : 0;
@@ -326,61 +405,130 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
     const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
     const int myv = nxt;
     if (!pk) nxt = base + 32 + lane < se ? ld_idx(a.idx + base + 32 + lane) : 0;
-#pragma unroll 1
-    for (int j0 = 0; j0 < cntw; j0 += ep * U) {
-      bool ok[U];
-      T dov[U][NE], kv[U][NE];
-      Rec<T> rec[U];
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const int j = j0 + t * ep + js;
-        ok[t] = j < cnt;
-        const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
-        const int vv = ok[t] ? v : 0;
-#pragma unroll
-        for (int k = 0; k < CPL; ++k)
-          ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
-        if constexpr (VAR == GF_DOT) {
-#pragma unroll
+#if GF_FULL_CHUNK_B
+    // whole 32-edge chunks: mask-free copy of the edge loop (as the forward)
+    auto chunk = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T dov[U][NE], kv[U][NE];
+        Rec<T> rec[U];
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;
+          const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
+          const int vv = ok[t] ? v : 0;
+  #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
-        }
-        rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
-      }
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        T dp = T(0);
-#pragma unroll
-        for (int i = 0; i < NE; ++i) dp += dov[t][i] * vu[i];
-        dp = head_sum(dp, a.LPH);
-        T s, rk = T(1), pre = T(0);
-        if constexpr (VAR == GF_DOT) {
-          T d = T(0);
-#pragma unroll
-          for (int i = 0; i < NE; ++i) d += qu[i] * kv[t][i];
-          d = head_sum(d, a.LPH);
-          if (a.l2) {
-            rk = rec[t].aux;
-            d *= rq * rk;
+            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
+          if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
           }
-          s = a.scale * d;
-        } else {
-          pre = elu + rec[t].aux;
-          s = lrelu(pre, a.slope);
+          rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
         }
-        const T p = ok[t] ? prob(s, rec[t]) : T(0);
-        const T ds = p * (dp - rec[t].delta);
-#pragma unroll
-        for (int i = 0; i < NE; ++i) all[i] += p * dov[t][i];
-        if constexpr (VAR == GF_DOT) {
-          const T w = a.scale * ds * rk;
-#pragma unroll
-          for (int i = 0; i < NE; ++i) all[NE + i] += w * kv[t][i];
-        } else {
-          all[NE] += ds * lrelu_grad(pre, a.slope);
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          T dp = T(0);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) dp += dov[t][i] * vu[i];
+          dp = head_sum(dp, a.LPH);
+          T s, rk = T(1), pre = T(0);
+          if constexpr (VAR == GF_DOT) {
+            T d = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) d += qu[i] * kv[t][i];
+            d = head_sum(d, a.LPH);
+            if (a.l2) {
+              rk = rec[t].aux;
+              d *= rq * rk;
+            }
+            s = a.scale * d;
+          } else {
+            pre = elu + rec[t].aux;
+            s = lrelu(pre, a.slope);
+          }
+          const T p = ok[t] ? prob(s, rec[t]) : T(0);
+          const T ds = p * (dp - rec[t].delta);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) all[i] += p * dov[t][i];
+          if constexpr (VAR == GF_DOT) {
+            const T w = a.scale * ds * rk;
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) all[NE + i] += w * kv[t][i];
+          } else {
+            all[NE] += ds * lrelu_grad(pre, a.slope);
+          }
+        }
+      }
+    };
+    if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
+      chunk(std::true_type{});
+    else
+      chunk(std::false_type{});
+#else
+    {
+      constexpr bool FULL = false;
+  #pragma unroll 1
+      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+        bool ok[U];
+        T dov[U][NE], kv[U][NE];
+        Rec<T> rec[U];
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          ok[t] = FULL || j < cnt;
+          const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
+          const int vv = ok[t] ? v : 0;
+  #pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
+          if constexpr (VAR == GF_DOT) {
+  #pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
+          }
+          rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          T dp = T(0);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) dp += dov[t][i] * vu[i];
+          dp = head_sum(dp, a.LPH);
+          T s, rk = T(1), pre = T(0);
+          if constexpr (VAR == GF_DOT) {
+            T d = T(0);
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) d += qu[i] * kv[t][i];
+            d = head_sum(d, a.LPH);
+            if (a.l2) {
+              rk = rec[t].aux;
+              d *= rq * rk;
+            }
+            s = a.scale * d;
+          } else {
+            pre = elu + rec[t].aux;
+            s = lrelu(pre, a.slope);
+          }
+          const T p = ok[t] ? prob(s, rec[t]) : T(0);
+          const T ds = p * (dp - rec[t].delta);
+  #pragma unroll
+          for (int i = 0; i < NE; ++i) all[i] += p * dov[t][i];
+          if constexpr (VAR == GF_DOT) {
+            const T w = a.scale * ds * rk;
+  #pragma unroll
+            for (int i = 0; i < NE; ++i) all[NE + i] += w * kv[t][i];
+          } else {
+            all[NE] += ds * lrelu_grad(pre, a.slope);
+          }
         }
       }
     }
+#endif
     if (pk) break;
   }
 
