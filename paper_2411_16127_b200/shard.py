@@ -157,8 +157,11 @@ class PeerTables:
         total = n * sum(widths.values())
         self.buf = symm_mem.empty(total, dtype=dtype, device=device)
         self.hdl = symm_mem.rendezvous(self.buf, group)
+        # the tensor's place inside the symmetric allocation (same on every rank)
+        self.storage_offset = int(getattr(self.hdl, "offset", 0)) // self.buf.element_size()
         self.peer_bufs = [self.buf if k == shard.rank else
-                          self.hdl.get_buffer(k, (total,), dtype, 0) for k in range(shard.world)]
+                          self.hdl.get_buffer(k, (total,), dtype, self.storage_offset)
+                          for k in range(shard.world)]
         self.offsets = {}
         off = 0
         for name, w in widths.items():

@@ -88,6 +88,10 @@ def test_peer_tables_gemm_bcast_world1(cuda):
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)  # noqa: E731
         sh = RowShard.build(g.n, t(g.row_ptr), t(g.col), t(g.csc_ptr), t(g.csc_row), 0, 1)
         pt = PeerTables(sh, {"Q": 64, "V": 128}, device=cuda)
+        # the peer-view addressing (get_buffer + storage offset) resolves to the
+        # tensor itself for the own rank
+        own = pt.hdl.get_buffer(0, (pt.buf.numel(),), pt.buf.dtype, pt.storage_offset)
+        assert own.data_ptr() == pt.buf.data_ptr()
         X = torch.rand(sh.n_padded, 32, device=cuda)
         Wq, Wv = torch.rand(32, 64, device=cuda), torch.rand(32, 128, device=cuda)
         pt.barrier()
