@@ -36,6 +36,10 @@
 #define GF_FULL_CHUNK_B 1
 #endif
 
+#ifndef GF_FULL_STEPS
+#define GF_FULL_STEPS 0
+#endif
+
 namespace gfb {
 
 namespace {
@@ -174,10 +178,10 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
     }
 #if GF_FULL_CHUNK_A
     // whole 32-edge chunks: mask-free copy of the edge loop (as the forward)
-    auto chunk = [&](auto full_tag) {
+    auto chunk = [&](auto full_tag, const int jb, const int je) {
       constexpr bool FULL = decltype(full_tag)::value;
   #pragma unroll 1
-      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+      for (int j0 = jb; j0 < je; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], el[U];
   #pragma unroll
@@ -233,10 +237,22 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
         }
       }
     };
+#if GF_FULL_STEPS
+    // every step whose U slots all lie inside the chunk runs mask-free (rows
+    // shorter than a chunk too); the remainder runs masked
+    if (!pk && CPL == 1) {
+      const int fe = cnt / (ep * U) * (ep * U);
+      if (fe > 0) chunk(std::true_type{}, 0, fe);
+      if (fe < cntw) chunk(std::false_type{}, fe, cntw);
+    } else {
+      chunk(std::false_type{}, 0, cntw);
+    }
+#else
     if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
-      chunk(std::true_type{});
+      chunk(std::true_type{}, 0, cntw);
     else
-      chunk(std::false_type{});
+      chunk(std::false_type{}, 0, cntw);
+#endif
 #else
     {
       constexpr bool FULL = false;
@@ -407,10 +423,10 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
     if (!pk) nxt = base + 32 + lane < se ? ld_idx(a.idx + base + 32 + lane) : 0;
 #if GF_FULL_CHUNK_B
     // whole 32-edge chunks: mask-free copy of the edge loop (as the forward)
-    auto chunk = [&](auto full_tag) {
+    auto chunk = [&](auto full_tag, const int jb, const int je) {
       constexpr bool FULL = decltype(full_tag)::value;
   #pragma unroll 1
-      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+      for (int j0 = jb; j0 < je; j0 += ep * U) {
         bool ok[U];
         T dov[U][NE], kv[U][NE];
         Rec<T> rec[U];
@@ -465,10 +481,22 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
         }
       }
     };
+#if GF_FULL_STEPS
+    // every step whose U slots all lie inside the chunk runs mask-free (rows
+    // shorter than a chunk too); the remainder runs masked
+    if (!pk && CPL == 1) {
+      const int fe = cnt / (ep * U) * (ep * U);
+      if (fe > 0) chunk(std::true_type{}, 0, fe);
+      if (fe < cntw) chunk(std::false_type{}, fe, cntw);
+    } else {
+      chunk(std::false_type{}, 0, cntw);
+    }
+#else
     if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
-      chunk(std::true_type{});
+      chunk(std::true_type{}, 0, cntw);
     else
-      chunk(std::false_type{});
+      chunk(std::false_type{}, 0, cntw);
+#endif
 #else
     {
       constexpr bool FULL = false;

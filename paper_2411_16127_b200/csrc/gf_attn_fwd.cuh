@@ -32,6 +32,10 @@
 #define GF_FULL_CHUNK 1
 #endif
 
+#ifndef GF_FULL_STEPS
+#define GF_FULL_STEPS 0
+#endif
+
 namespace gfb {
 
 namespace {
@@ -133,10 +137,10 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
 #if GF_FULL_CHUNK
     // Whole 32-edge chunks (all but a row's last) run a mask-free copy of the
     // loop: no per-slot bounds compare / select on the ids and probabilities.
-    auto chunk = [&](auto full_tag) {
+    auto chunk = [&](auto full_tag, const int jb, const int je) {
       constexpr bool FULL = decltype(full_tag)::value;
   #pragma unroll 1
-      for (int j0 = 0; j0 < cntw; j0 += ep * U) {
+      for (int j0 = jb; j0 < je; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], s[U];
   #pragma unroll
@@ -209,10 +213,22 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
     };
     // (only when the loop's slots tile the chunk exactly — EPW * U divides 32 —
     // and for one-chunk lanes: the CPL = 2 shapes (GT 8x16) measured slower)
+#if GF_FULL_STEPS
+    // every step whose U slots all lie inside the chunk runs mask-free (rows
+    // shorter than a chunk too); the remainder runs masked
+    if (!pk && CPL == 1) {
+      const int fe = cnt / (ep * U) * (ep * U);
+      if (fe > 0) chunk(std::true_type{}, 0, fe);
+      if (fe < cntw) chunk(std::false_type{}, fe, cntw);
+    } else {
+      chunk(std::false_type{}, 0, cntw);
+    }
+#else
     if (!pk && CPL == 1 && (32 % (EPW * U)) == 0 && cnt == 32)
-      chunk(std::true_type{});
+      chunk(std::true_type{}, 0, cntw);
     else
-      chunk(std::false_type{});
+      chunk(std::false_type{}, 0, cntw);
+#endif
 #else
     {
       constexpr bool FULL = false;
