@@ -450,6 +450,7 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
 
                 pt = PeerTables(shard, {"V": F} if gat_layer(layer) else {"Q": F, "K": F, "V": F},
                                 device=dev)
+                pt.selftest()
                 exchange = "p2p: gemm_bcast epilogue into symmetric-memory tables + device barrier"
             except Exception as ex:  # recorded in the JSON line, NCCL path used
                 exchange = f"nccl (p2p unavailable: {type(ex).__name__}: {str(ex)[:120]})"

@@ -180,6 +180,24 @@ class PeerTables:
         """gemm_bcast destinations of this rank's block (own first)."""
         return block_views([self._table(b, name) for b in self.peer_bufs], self.shard)
 
+    def selftest(self):
+        """End-to-end check of the peer addressing: every rank writes rank+1
+        into its block of every copy of the first table, barrier, and every
+        block of the local copy must then hold its owner's value.  Raises on a
+        mismatch (the caller falls back to the NCCL exchange)."""
+        name = next(iter(self.offsets))
+        R = self.shard.R
+        t = self.table(name)
+        self.barrier()
+        for d in self.dests(name):
+            d.fill_(float(self.shard.rank + 1))
+        self.barrier()
+        got = t.view(self.shard.world, R, -1)[:, :, 0].cpu()
+        want = torch.arange(1, self.shard.world + 1, dtype=got.dtype)[:, None].expand_as(got)
+        if not torch.equal(got, want):
+            raise RuntimeError("PeerTables.selftest: peer writes did not land in every copy")
+        self.barrier()
+
     def barrier(self):
         """Device-side barrier on the current stream: every rank's writes
         issued before it are visible to every rank after it."""

@@ -92,6 +92,7 @@ def test_peer_tables_gemm_bcast_world1(cuda):
         # tensor itself for the own rank
         own = pt.hdl.get_buffer(0, (pt.buf.numel(),), pt.buf.dtype, pt.storage_offset)
         assert own.data_ptr() == pt.buf.data_ptr()
+        pt.selftest()
         X = torch.rand(sh.n_padded, 32, device=cuda)
         Wq, Wv = torch.rand(32, 64, device=cuda), torch.rand(32, 128, device=cuda)
         pt.barrier()
