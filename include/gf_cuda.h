@@ -106,7 +106,9 @@ int gf_stream_sync(void* stream);
  * From the reference's canonical host arrays (int64, as in graphfuse::Graph);
  * the CSC edge permutation is not needed on the device (the backward
  * recomputes attention instead of indexing a stored P).  cta_threshold <= 0
- * selects the default.  Synchronises `stream` once (schedule build). */
+ * selects the automatic threshold clamp(E / 28416, 1024, 16384) (a row gets
+ * a whole CTA once it holds ~1/8 of one resident warp's share of the edges).
+ * Synchronises `stream` once (schedule build). */
 int gf_graph_create(int64_t num_nodes, int64_t num_edges, const int64_t* csr_row_ptr,
                     const int64_t* csr_col_idx, const int64_t* csc_col_ptr,
                     const int64_t* csc_row_idx, int32_t cta_threshold, void* stream,

@@ -125,7 +125,7 @@ int build_sched(const int32_t* order, const int32_t* ptr, int n, int4** out, cud
 }
 
 int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
-  g->cta_threshold = thr > 0 ? thr : kDefaultCtaThreshold;
+  g->cta_threshold = thr > 0 ? thr : auto_cta_threshold(std::max<int64_t>(g->e, g->e_csc));
   GF_CHECK_CUDA(cudaGetDevice(&g->device));
   GF_CHECK_CUDA(cudaMalloc(&g->row_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));
   GF_CHECK_CUDA(cudaMalloc(&g->col_order, sizeof(int32_t) * (g->n > 0 ? g->n : 1)));

@@ -126,7 +126,16 @@ struct DevGraph {
 #define GF_U2 1
 #endif
 
-constexpr int kDefaultCtaThreshold = 1024;
+constexpr int kDefaultCtaThreshold = 1024;  // floor of the automatic threshold
+// Automatic CTA-row threshold: a row gets a whole CTA once it holds more than
+// ~1/8 of the edges one resident warp processes over the kernel (E / (148 SMs
+// x 24 warps)), so no single warp row outlasts the launch, while rows below
+// that keep the cheaper warp path (C4 sweep, profiles/ab_r1_cta_threshold.txt:
+// 1024 -> 17.1, 3072-16384 -> 17.4-17.7 GEdges/s).  Clamped to [1024, 16384].
+inline int auto_cta_threshold(int64_t e) {
+  const int64_t t = e / (148 * 24 * 8);
+  return static_cast<int>(t < kDefaultCtaThreshold ? kDefaultCtaThreshold : (t > 16384 ? 16384 : t));
+}
 constexpr int kSmallDegree = 8;  // packed (sub-warp) bucket: degree 1..8
 
 // Warp-bucket rows per warp: software-pipelined row prologues pay off for
