@@ -1132,7 +1132,8 @@ def run_ours(args, rank, world):
             "layer": layer_out,
             "fwd_strategy_ms": ablation,
             "bwd_strategy_ms": bwd_ablation,
-            "gpu_launches": 3 * args.steps,
+            # fwd (or one per source block + the merge when phased), pass A, pass B
+            "gpu_launches": ((world + 1) if phased else 1) * args.steps + 2 * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))
