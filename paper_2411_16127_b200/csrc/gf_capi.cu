@@ -1,3 +1,7 @@
+#include <atomic>
+#include <algorithm>
+#include <mutex>
+#include <cstdlib>
 // C-ABI entry points of libgraphfuse_cuda (see include/gf_cuda.h).
 #include <string>
 
@@ -157,8 +161,60 @@ bool bad_graph(gf_graph_t g, const char* who) {
 
 }  // namespace
 
+// L2 carve-out for the evict-last node tables.  The kernels mark the gathered
+// tables (V, Q|el, dO, K, records) L2::evict_last and the streamed ids
+// evict_first; measured on B200, that priority only protects lines while a
+// persisting-L2 set-aside exists (cudaLimitPersistingL2CacheSize; 0 by
+// default).  With a 64 MiB set-aside C4 (gathered tables 67-90 MB) runs
+// 17.6 -> 18.2 GEdges/s; with tables far beyond L2 (C5) it is neutral
+// (profiles/ab_r1_l2_persist.txt).  So when a pass's gathered tables are at
+// most 128 MiB, the limit is raised (never lowered) to 64 MiB, capped at the
+// device maximum.  GF_L2_SETASIDE=<MiB> overrides the size; 0 disables.
+static void ensure_l2_setaside(int64_t gathered_bytes) {
+  static const long env = [] {
+    const char* e = std::getenv("GF_L2_SETASIDE");
+    return e && *e ? std::atol(e) : -1L;
+  }();
+  if (env == 0) return;
+  if (env < 0 && gathered_bytes > (int64_t(128) << 20)) return;
+  static std::atomic<uint32_t> applied{0};  // bit d: device d done (one query, one set)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) {
+    cudaGetLastError();
+    return;
+  }
+  if (applied.load(std::memory_order_acquire) >> dev & 1u) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (applied.load() >> dev & 1u) return;
+  applied.fetch_or(1u << dev);
+  int max_persist = 0;
+  size_t cur = 0;
+  if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const size_t want = std::min(static_cast<size_t>(env > 0 ? env : 64) << 20,
+                               static_cast<size_t>(max_persist));
+  if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
+    cudaGetLastError();  // best effort: never fail the call over the cache hint
+}
+
+// gathered node-table bytes of one pass (fwd / pass A: V + Q|el; pass B:
+// dO + records [+ K for dot models])
+static int64_t gathered_bytes(const gf_graph_s* g, const gf_attn_desc* d, int pass) {
+  const int64_t F = static_cast<int64_t>(d->heads) * d->head_dim;
+  const int64_t qk = d->variant == GF_DOT ? F : d->heads;
+  const int64_t b = d->dtype == GF_F32 ? 4 : 8;
+  const int64_t n = g->n;
+  return pass == 2 ? n * b * (F + 4 * d->heads + (d->variant == GF_DOT ? F : 0))
+                   : n * b * (F + qk);
+}
+
 extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                            const void* V, void* O, void* stats, void* P, void* stream) {
+  ensure_l2_setaside(gathered_bytes(g, desc, 0));
   if (int rc = check_desc(desc, "gf_attn_fwd")) return rc;
   if (bad_graph(g, "gf_attn_fwd")) return GF_ERR_INVALID;
   if (g->n > 0 && (!Q || !K || !V || !O || !stats)) {
@@ -265,6 +321,7 @@ extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q
     gfb::set_error("gf_attn_bwd: null operand");
     return GF_ERR_INVALID;
   }
+  ensure_l2_setaside(gathered_bytes(g, desc, 1));
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
              ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, dQ, dK, dV, 3, s)
@@ -280,6 +337,7 @@ extern "C" int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const vo
     gfb::set_error("gf_attn_bwd_rows: null operand");
     return GF_ERR_INVALID;
   }
+  ensure_l2_setaside(gathered_bytes(g, desc, 1));
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
              ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, 1, s)
@@ -295,6 +353,7 @@ extern "C" int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const vo
     gfb::set_error("gf_attn_bwd_cols: null operand");
     return GF_ERR_INVALID;
   }
+  ensure_l2_setaside(gathered_bytes(g, desc, 2));
   auto s = static_cast<cudaStream_t>(stream);
   void* st = const_cast<void*>(stats);
   return desc->dtype == GF_F32
