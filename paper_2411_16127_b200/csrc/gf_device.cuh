@@ -235,12 +235,20 @@ struct Rec {
   T m, ll2, aux, delta;
 };
 
+#ifndef GF_REC_KEEP
+#define GF_REC_KEEP 0  // 1: records also evict_last (dO alone fits the 64 MiB carve-out)
+#endif
 template <typename T>
 __device__ __forceinline__ Rec<T> ld_rec(const T* __restrict__ st, size_t i) {
   Rec<T> r;
   if constexpr (sizeof(T) == 4) {
     float x[4];
+#if GF_REC_KEEP
     ld_gather<float, 16>(st + 4 * i, x);
+#else
+    const float4 v = __ldg(reinterpret_cast<const float4*>(st + 4 * i));
+    x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+#endif
     r.m = x[0], r.ll2 = x[1], r.aux = x[2], r.delta = x[3];
   } else {
     double x[4];
