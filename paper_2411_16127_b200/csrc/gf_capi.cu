@@ -214,13 +214,13 @@ static int64_t gathered_bytes(const gf_graph_s* g, const gf_attn_desc* d, int pa
 
 extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                            const void* V, void* O, void* stats, void* P, void* stream) {
-  ensure_l2_setaside(gathered_bytes(g, desc, 0));
   if (int rc = check_desc(desc, "gf_attn_fwd")) return rc;
   if (bad_graph(g, "gf_attn_fwd")) return GF_ERR_INVALID;
   if (g->n > 0 && (!Q || !K || !V || !O || !stats)) {
     gfb::set_error("gf_attn_fwd: null operand");
     return GF_ERR_INVALID;
   }
+  ensure_l2_setaside(gathered_bytes(g, desc, 0));  // after validation: g is a live graph
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32 ? fwd_impl<float>(g, *desc, Q, K, V, O, stats, P, s)
                                : fwd_impl<double>(g, *desc, Q, K, V, O, stats, P, s);
