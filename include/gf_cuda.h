@@ -285,6 +285,23 @@ int gf_gen_molecules_device(int64_t mols, int64_t atoms, int64_t rings, uint64_t
                             int64_t capacity, int64_t* src, int64_t* dst, int64_t* e_out,
                             void* stream);
 
+/* ---- device-wide state (opt-in; the library never changes it on its own) ----
+ * gf_l2_persist(bytes): set cudaLimitPersistingL2CacheSize of the current
+ * device to min(bytes, device max).  The kernels tag the gathered node
+ * tables L2::evict_last, which keeps them resident only while a set-aside
+ * exists (C4: +2-3 %).  bytes = 0 first demotes every persisting line
+ * (cudaCtxResetPersistingL2Cache) and then removes the set-aside.
+ * GF_L2_SETASIDE=<MiB> in the environment opts in at the first attention
+ * call instead.  gf_l2_persist_get reads the current limit.
+ * gf_l2_reset_persisting(): demote every persisting line to normal (e.g.
+ * before a cold-L2 timing step), keeping the set-aside.
+ * gf_scratch_trim(): synchronise the device and release the stream-ordered
+ * scratch the library caches in its private memory pool. */
+int gf_l2_persist(size_t bytes);
+int gf_l2_persist_get(size_t* bytes);
+int gf_l2_reset_persisting(void);
+int gf_scratch_trim(void);
+
 /* ---- diagnostics ----
  * Measured gather bandwidth (GB/s) of rows of row_bytes (32..1024, lanes read
  * consecutive 32 B chunks with 256-bit non-coherent loads) chosen in hashed

@@ -108,6 +108,12 @@ def ref():
         _ref.gfref_time_head_f32.restype = C.c_int
         _ref.gfref_time_head_f32.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double,
                                              C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        _ref.gfref_time_step_f32.restype = C.c_int
+        _ref.gfref_time_step_f32.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_double,
+                                             C.c_double, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        _ref.gfref_time_conv_f32.restype = C.c_int
+        _ref.gfref_time_conv_f32.argtypes = [_vp, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                             C.c_double, C.c_double] + [_vp] * 8
         _ref.gfref_forward_counters.restype = C.c_int
         _ref.gfref_forward_counters.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                                 C.c_int64, C.c_int64, C.c_int64, C.c_int64,

@@ -11,6 +11,7 @@
 //              (module.cpp:120-130: P = edge_softmax(sddmm(Q, K))).
 //   layer    = graphfuse::conv_forward / conv_backward (models.hpp:104-158)
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg load it.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -162,6 +163,101 @@ int time_head_impl(const gf::Graph* g, int D, int variant, double scale, double 
   }
 }
 
+// Timing leg of the reference arm: one whole multi-head layer step, every
+// head h = 0..H-1 through run_strategy<T> then fused_backward<T> (the
+// reference is single-head, so a multi-head user slices columns
+// per head).  Only the reference calls are timed; the column slicing is not.
+template <typename T>
+int time_step_impl(const gf::Graph* g, int H, int D, int variant, double scale, double slope,
+                   int l2, const T* Q, const T* K, const T* V, const T* dO, double* fwd_s,
+                   double* bwd_s) {
+  try {
+    Shape sh = shape_of(*g, H, D, variant);
+    gf::FusionPlan plan;
+    plan.dtype_bytes = sizeof(T);
+    plan.shared_mem_budget_bytes = std::int64_t(1) << 30;  // acceptance_main.cpp:46 precedent
+    auto kind = make_kind(variant, scale, slope, l2);
+    double f = 0, b = 0;
+    volatile T sink = 0;
+    for (int h = 0; h < H; ++h) {
+      auto q = slice(Q, sh.n, sh.qk_ld, h * sh.qk_w, sh.qk_w);
+      auto k = slice(K, sh.n, sh.qk_ld, h * sh.qk_w, sh.qk_w);
+      auto v = slice(V, sh.n, std::int64_t(H) * D, std::int64_t(h) * D, D);
+      auto d_o = slice(dO, sh.n, std::int64_t(H) * D, std::int64_t(h) * D, D);
+      auto t0 = std::chrono::steady_clock::now();
+      auto res = gf::run_strategy(*g, q, k, v, kind, plan);
+      auto t1 = std::chrono::steady_clock::now();
+      auto bw = gf::fused_backward(*g, res.ctx, d_o, plan);
+      auto t2 = std::chrono::steady_clock::now();
+      f += std::chrono::duration<double>(t1 - t0).count();
+      b += std::chrono::duration<double>(t2 - t1).count();
+      sink = res.O.data.empty() ? T(0) : res.O.data[0];
+      sink = bw.grads.dV.data.empty() ? T(0) : bw.grads.dV.data[0];
+    }
+    (void)sink;
+    *fwd_s = f;
+    *bwd_s = b;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Layer level (models.hpp:104-158), every head: conv_forward + conv_backward
+// with head h's weight columns (W[:, hD:(h+1)D], a_l/a_r[hD:(h+1)D]).  X is
+// N x d_in; dO is N x (H*D).  *pipe_s = the part of that time spent in
+// run_strategy + fused_backward (timed separately on the same inputs), so a
+// caller can split projection and pipeline cost.
+template <typename T>
+int time_conv_impl(const gf::Graph* g, int model, int H, std::int64_t D, std::int64_t d_in,
+                   double scale, double slope, const T* X, const T* Wq, const T* Wk, const T* Wv,
+                   const T* al, const T* ar, const T* dO, double* layer_s) {
+  try {
+    gf::ConvSpec spec;
+    spec.model = static_cast<gf::Model>(model);
+    spec.dim = D;
+    spec.scale = scale;
+    spec.leaky_slope = slope;
+    gf::DenseMatrix<T> x(g->num_nodes, d_in);
+    std::memcpy(x.data.data(), X, sizeof(T) * x.data.size());
+    gf::FusionPlan plan;
+    plan.dtype_bytes = sizeof(T);
+    plan.shared_mem_budget_bytes = std::int64_t(1) << 30;
+    const std::int64_t F = std::int64_t(H) * D;
+    double t = 0;
+    volatile T sink = 0;
+    for (int h = 0; h < H; ++h) {
+      gf::ConvWeights<T> w;
+      w.W_v = slice(Wv, d_in, F, h * D, D);
+      if (spec.model == gf::Model::GAT) {
+        gf::DenseMatrix<T> a(D, 1), b(D, 1);
+        for (std::int64_t i = 0; i < D; ++i) {
+          a.data[i] = al[h * D + i];
+          b.data[i] = ar[h * D + i];
+        }
+        w.a_l = a;
+        w.a_r = b;
+      } else {
+        w.W_q = slice(Wq, d_in, F, h * D, D);
+        w.W_k = slice(Wk, d_in, F, h * D, D);
+      }
+      auto d_o = slice(dO, g->num_nodes, F, h * D, D);
+      auto t0 = std::chrono::steady_clock::now();
+      auto [out, ctx] = gf::conv_forward(spec, *g, x, w, plan);
+      auto grads = gf::conv_backward(spec, *g, ctx, w, d_o);
+      auto t1 = std::chrono::steady_clock::now();
+      t += std::chrono::duration<double>(t1 - t0).count();
+      sink = out.data.empty() ? T(0) : out.data[0];
+      sink = grads.dW_v.data.empty() ? T(0) : grads.dW_v.data[0];
+    }
+    (void)sink;
+    *layer_s = t;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -264,6 +360,20 @@ int gfref_time_head_f32(void* g, int D, int variant, double scale, double slope,
                         double* fwd_s, double* bwd_s) {
   return time_head_impl<float>(static_cast<gf::Graph*>(g), D, variant, scale, slope, l2, Q, K,
                                V, dO, fwd_s, bwd_s);
+}
+
+int gfref_time_step_f32(void* g, int H, int D, int variant, double scale, double slope, int l2,
+                        const float* Q, const float* K, const float* V, const float* dO,
+                        double* fwd_s, double* bwd_s) {
+  return time_step_impl<float>(static_cast<gf::Graph*>(g), H, D, variant, scale, slope, l2, Q,
+                               K, V, dO, fwd_s, bwd_s);
+}
+int gfref_time_conv_f32(void* g, int model, int H, std::int64_t D, std::int64_t d_in,
+                        double scale, double slope, const float* X, const float* Wq,
+                        const float* Wk, const float* Wv, const float* al, const float* ar,
+                        const float* dO, double* layer_s) {
+  return time_conv_impl<float>(static_cast<gf::Graph*>(g), model, H, D, d_in, scale, slope, X,
+                               Wq, Wk, Wv, al, ar, dO, layer_s);
 }
 
 // Counters of one single-head forward (ExecCounters::to_map order, elapsed excluded):

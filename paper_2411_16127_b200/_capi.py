@@ -83,6 +83,10 @@ SIGNATURES = {
                                           _vp, _vp, C.POINTER(C.c_int64), _vp]),
     "gf_gen_molecules_device": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int64,
                                           _vp, _vp, C.POINTER(C.c_int64), _vp]),
+    "gf_l2_persist": (C.c_int, [C.c_size_t]),
+    "gf_l2_persist_get": (C.c_int, [C.POINTER(C.c_size_t)]),
+    "gf_l2_reset_persisting": (C.c_int, []),
+    "gf_scratch_trim": (C.c_int, []),
     "gf_measure_l2_gather": (C.c_int, [C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -13,21 +13,53 @@ thread_local std::string t_err;
 }
 void set_error(const std::string& msg) { t_err = msg; }
 
+namespace {
+std::once_flag pool_once[64];
+cudaMemPool_t pools[64];
+}  // namespace
+
 cudaError_t scratch_alloc_raw(void** p, size_t bytes, cudaStream_t s) {
-  static bool tuned[64] = {};
+  // Library-private stream-ordered pool per device: freed scratch stays
+  // mapped for the next call (with a release threshold of 0 every
+  // synchronisation returned it and the next call re-mapped it: +5.6 ms per
+  // unfused AGNN backward on C3), without touching the device's default pool
+  // that the host application (e.g. PyTorch) allocates from.
+  // gf_scratch_trim() gives the cached bytes back.
   int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !tuned[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+  std::call_once(pool_once[dev], [dev] {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
       uint64_t keep = uint64_t(8) << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = pool;
+    } else {
+      cudaGetLastError();
     }
-    tuned[dev] = true;
-  }
-  return cudaMallocAsync(p, bytes, s);
+  });
+  if (!pools[dev]) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pools[dev], s);
 }
+
+cudaMemPool_t scratch_pool(int dev) { return dev >= 0 && dev < 64 ? pools[dev] : nullptr; }
 }  // namespace gfb
 
+
+extern "C" int gf_scratch_trim(void) {
+  int dev = 0;
+  GF_CHECK_CUDA(cudaGetDevice(&dev));
+  if (cudaMemPool_t pool = gfb::scratch_pool(dev)) {
+    GF_CHECK_CUDA(cudaDeviceSynchronize());
+    GF_CHECK_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
+  return GF_OK;
+}
 
 extern "C" const char* gf_last_error(void) { return gfb::t_err.c_str(); }
 
@@ -161,55 +193,55 @@ bool bad_graph(gf_graph_t g, const char* who) {
 
 }  // namespace
 
-// L2 carve-out for the evict-last node tables.  The kernels mark the gathered
-// tables (V, Q|el, dO, K, records) L2::evict_last and the streamed ids
+// L2 carve-out for the evict-last node tables (opt-in).  The kernels mark the
+// gathered tables (V, Q|el, dO, K) L2::evict_last and the streamed ids
 // evict_first; measured on B200, that priority only protects lines while a
 // persisting-L2 set-aside exists (cudaLimitPersistingL2CacheSize; 0 by
-// default).  With a 64 MiB set-aside C4 (gathered tables 67-90 MB) runs
-// 17.6 -> 18.2 GEdges/s; with tables far beyond L2 (C5) it is neutral
-// (profiles/ab_r1_l2_persist.txt).  So when a pass's gathered tables are at
-// most 128 MiB, the limit is raised (never lowered) to 64 MiB, capped at the
-// device maximum.  GF_L2_SETASIDE=<MiB> overrides the size; 0 disables.
-static void ensure_l2_setaside(int64_t gathered_bytes) {
+// default).  With a 64 MiB set-aside C4 (gathered tables 67-90 MB) gains
+// ~2-3 %; with tables far beyond L2 (C5) it is neutral
+// (profiles/ab_r1_l2_persist.txt).  The set-aside is a device-wide limit, so
+// the library never changes it on its own: a caller opts in with
+// gf_l2_persist(bytes) (bench.py does) or GF_L2_SETASIDE=<MiB> in the
+// environment, and gf_l2_persist(0) / gf_l2_reset_persisting() give the
+// lines back.
+static void ensure_l2_setaside() {
   static const long env = [] {
     const char* e = std::getenv("GF_L2_SETASIDE");
-    return e && *e ? std::atol(e) : -1L;
+    return e && *e ? std::atol(e) : 0L;
   }();
-  if (env == 0) return;
-  if (env < 0 && gathered_bytes > (int64_t(128) << 20)) return;
-  static std::atomic<uint32_t> applied{0};  // bit d: device d done (one query, one set)
+  if (env <= 0) return;
+  static std::atomic<uint32_t> applied{0};  // bit d: device d done
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) {
     cudaGetLastError();
     return;
   }
-  if (applied.load(std::memory_order_acquire) >> dev & 1u) return;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  if (applied.load() >> dev & 1u) return;
-  applied.fetch_or(1u << dev);
-  int max_persist = 0;
-  size_t cur = 0;
-  if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  const size_t want = std::min(static_cast<size_t>(env > 0 ? env : 64) << 20,
-                               static_cast<size_t>(max_persist));
-  if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
-    cudaGetLastError();  // best effort: never fail the call over the cache hint
+  if (applied.fetch_or(1u << dev) >> dev & 1u) return;
+  gf_l2_persist(static_cast<size_t>(env) << 20);
 }
 
-// gathered node-table bytes of one pass (fwd / pass A: V + Q|el; pass B:
-// dO + records [+ K for dot models])
-static int64_t gathered_bytes(const gf_graph_s* g, const gf_attn_desc* d, int pass) {
-  const int64_t F = static_cast<int64_t>(d->heads) * d->head_dim;
-  const int64_t qk = d->variant == GF_DOT ? F : d->heads;
-  const int64_t b = d->dtype == GF_F32 ? 4 : 8;
-  const int64_t n = g->n;
-  return pass == 2 ? n * b * (F + 4 * d->heads + (d->variant == GF_DOT ? F : 0))
-                   : n * b * (F + qk);
+extern "C" int gf_l2_persist(size_t bytes) {
+  int dev = 0, max_persist = 0;
+  GF_CHECK_CUDA(cudaGetDevice(&dev));
+  GF_CHECK_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  if (bytes == 0) GF_CHECK_CUDA(cudaCtxResetPersistingL2Cache());
+  GF_CHECK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                   std::min(bytes, static_cast<size_t>(max_persist))));
+  return GF_OK;
+}
+
+extern "C" int gf_l2_persist_get(size_t* bytes) {
+  if (!bytes) {
+    gfb::set_error("gf_l2_persist_get: null out");
+    return GF_ERR_INVALID;
+  }
+  GF_CHECK_CUDA(cudaDeviceGetLimit(bytes, cudaLimitPersistingL2CacheSize));
+  return GF_OK;
+}
+
+extern "C" int gf_l2_reset_persisting(void) {
+  GF_CHECK_CUDA(cudaCtxResetPersistingL2Cache());
+  return GF_OK;
 }
 
 extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
@@ -220,7 +252,7 @@ extern "C" int gf_attn_fwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q
     gfb::set_error("gf_attn_fwd: null operand");
     return GF_ERR_INVALID;
   }
-  ensure_l2_setaside(gathered_bytes(g, desc, 0));  // after validation: g is a live graph
+  ensure_l2_setaside();
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32 ? fwd_impl<float>(g, *desc, Q, K, V, O, stats, P, s)
                                : fwd_impl<double>(g, *desc, Q, K, V, O, stats, P, s);
@@ -321,7 +353,7 @@ extern "C" int gf_attn_bwd(gf_graph_t g, const gf_attn_desc* desc, const void* Q
     gfb::set_error("gf_attn_bwd: null operand");
     return GF_ERR_INVALID;
   }
-  ensure_l2_setaside(gathered_bytes(g, desc, 1));
+  ensure_l2_setaside();
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
              ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, dQ, dK, dV, 3, s)
@@ -337,7 +369,7 @@ extern "C" int gf_attn_bwd_rows(gf_graph_t g, const gf_attn_desc* desc, const vo
     gfb::set_error("gf_attn_bwd_rows: null operand");
     return GF_ERR_INVALID;
   }
-  ensure_l2_setaside(gathered_bytes(g, desc, 1));
+  ensure_l2_setaside();
   auto s = static_cast<cudaStream_t>(stream);
   return desc->dtype == GF_F32
              ? bwd_impl<float>(g, *desc, Q, K, V, O, stats, dO, nullptr, dK, nullptr, 1, s)
@@ -353,7 +385,7 @@ extern "C" int gf_attn_bwd_cols(gf_graph_t g, const gf_attn_desc* desc, const vo
     gfb::set_error("gf_attn_bwd_cols: null operand");
     return GF_ERR_INVALID;
   }
-  ensure_l2_setaside(gathered_bytes(g, desc, 2));
+  ensure_l2_setaside();
   auto s = static_cast<cudaStream_t>(stream);
   void* st = const_cast<void*>(stats);
   return desc->dtype == GF_F32

@@ -105,3 +105,29 @@ def test_gen_molecules_device_errors(cuda):
 
     with pytest.raises(Exception, match="gen_molecules"):
         fused.gen_molecules_device(0, 26, 3)
+
+
+@pytest.mark.parametrize("name", ["cora", "pubmed", "molhiv", "reddit_slice", "power_law_small"])
+def test_host_generator_port_is_bit_exact(cuda, name):
+    """bench.py's numpy restatement of the device generators (the reference
+    arm's graphs) produces the SAME edge list as the device generator, so the
+    CPU reference and the GPU path time one graph."""
+    import bench
+    from paper_2411_16127_b200 import fused
+
+    if name == "reddit_slice":
+        rows = bench.REDDIT_N // 128
+        n, s_h, d_h = bench.gen_graph_host("reddit", rows=rows)
+        _, s_d, d_d = bench.gen_graph_device("reddit", torch.device("cuda"))
+        keep = d_d < rows
+        s_d, d_d = s_d[keep], d_d[keep]
+    elif name == "power_law_small":
+        n = 20_000
+        s_h, d_h = bench.host_power_law(n, 2_000, 0.34, seed=3)
+        s_d, d_d = fused.gen_power_law_device(n, 2_000, 0.34, seed=3)
+    else:
+        n, s_h, d_h = bench.gen_graph_host(name)
+        _, s_d, d_d = bench.gen_graph_device(name, torch.device("cuda"))
+    assert len(s_h) > 0
+    np.testing.assert_array_equal(s_d.cpu().numpy(), s_h)
+    np.testing.assert_array_equal(d_d.cpu().numpy(), d_h)
