@@ -206,6 +206,17 @@ int gf_softmax_backward(gf_graph_t g, int32_t dtype, int32_t heads, const void* 
 int gf_sddmm_backward(gf_graph_t g, const gf_attn_desc* desc, const void* Q, const void* K,
                       const void* dS, void* dQ, void* dK, void* stream);
 
+/* dense_oracle_forward (kernels.hpp:122-166), single head: the reference's
+ * masked dense test oracle on the device.  S (n x n, caller-allocated,
+ * row-major) gets S[v*n+u] = score of edge u -> v and 0 off the mask; O
+ * (n x v_cols) = row softmax over the mask (u ascending) times V, densely.
+ * desc: heads = 1, head_dim = Q/K width (1 for GF_ADD), scale / slope / l2 as
+ * in SddmmKind.  coo_src/coo_dst: device int64 [e] (the Graph's COO).
+ * n > 4096 -> GF_ERR_INVALID ("dense_oracle_forward: N > 4096"). */
+int gf_dense_oracle_forward(int64_t n, int64_t e, const int64_t* coo_src, const int64_t* coo_dst,
+                            const gf_attn_desc* desc, int64_t v_cols, const void* Q,
+                            const void* K, const void* V, void* S, void* O, void* stream);
+
 /* ---- recompute backward (replaces backward_values, autograd.hpp:158-170) ----
  * Pass A over CSR rows (dK or der, and delta into stats), pass B over CSC
  * columns (dQ or del, dV).  Attention is recomputed from the stats records;

@@ -136,6 +136,13 @@ bool all_finite(const DenseMatrix<T>& m) {
   return true;
 }
 
+template <typename T>
+bool all_finite(const EdgeScalars<T>& s) {
+  for (T v : s.values)
+    if (!std::isfinite(v)) return false;
+  return true;
+}
+
 /// Uniform [lo, hi) fixture matrix from mt19937_64 (same stream as dense.hpp:78-86).
 template <typename T>
 DenseMatrix<T> random_matrix(std::int64_t rows, std::int64_t cols, std::uint64_t seed,
@@ -287,9 +294,11 @@ ForwardResult<T> run_strategy(const Graph& g, const DenseMatrix<T>& Q, const Den
 
 // ----------------------------------------------------------- kernels.hpp --
 // Single-step operators (kernels.hpp:18-117), each one device op
-// (gf_sddmm / gf_edge_softmax / gf_spmm / gf_l2_normalize_rows).  The dense
-// masked test oracle dense_oracle_forward (kernels.hpp:122-166) is test
-// infrastructure and lives with the other CPU checkers under oracle/.
+// (gf_sddmm / gf_edge_softmax / gf_spmm / gf_l2_normalize_rows), and the
+// reference's masked dense oracle dense_oracle_forward (kernels.hpp:122-166)
+// as a dense device op (gf_dense_oracle_forward; N <= 4096, KernelError
+// "dense_oracle_forward: N > 4096" otherwise).  Returns (S_dense, O) with
+// S_dense[v][u] the score of edge u -> v.
 template <typename T>
 EdgeScalars<T> sddmm_dot(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
                          T scale);
@@ -305,6 +314,12 @@ DenseMatrix<T> spmm(const Graph& g, const EdgeScalars<T>& p, const DenseMatrix<T
 template <typename T>
 EdgeScalars<T> sddmm(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<T>& K,
                      const SddmmKind& kind);
+template <typename T>
+std::pair<DenseMatrix<T>, DenseMatrix<T>> dense_oracle_forward(const Graph& g,
+                                                               const DenseMatrix<T>& Q,
+                                                               const DenseMatrix<T>& K,
+                                                               const DenseMatrix<T>& V,
+                                                               const SddmmKind& kind);
 
 // --------------------------------------------------------------- autograd --
 template <typename T>

@@ -83,6 +83,8 @@ SIGNATURES = {
                                           _vp, _vp, C.POINTER(C.c_int64), _vp]),
     "gf_gen_molecules_device": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int64,
                                           _vp, _vp, C.POINTER(C.c_int64), _vp]),
+    "gf_dense_oracle_forward": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, C.POINTER(AttnDesc),
+                                          C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gf_l2_persist": (C.c_int, [C.c_size_t]),
     "gf_l2_persist_get": (C.c_int, [C.POINTER(C.c_size_t)]),
     "gf_l2_reset_persisting": (C.c_int, []),

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <algorithm>
 #include <limits>
+#include <mutex>
 
 #include "gf_cuda.h"
 #include "graphfuse/graphfuse.hpp"
@@ -62,17 +63,27 @@ struct DeviceGraphCache {
   EdgeId e = -1;
   const void* row_data = nullptr;
   const void* col_data = nullptr;
+  const void* csc_ptr_data = nullptr;
+  const void* csc_row_data = nullptr;
   std::int64_t thr = 0;
   ~DeviceGraphCache() {
     if (h) gf_graph_destroy(h);
   }
 };
 
+// The device copy is keyed on the Graph's sizes, the addresses of all four
+// topology arrays and the CTA threshold.  Like the reference's Graph (SPEC:
+// immutable, shareable), a Graph must not be edited in place after its first
+// device call; concurrent callers on one Graph are serialised by the mutex
+// while the cache is checked or rebuilt.
 gf_graph_t device_graph(const Graph& g, const FusionPlan& plan) {
   need_device();
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   auto& c = g.device;
   if (!c || c->n != g.num_nodes || c->e != g.num_edges ||
       c->row_data != g.csr_row_ptr.data() || c->col_data != g.csr_col_idx.data() ||
+      c->csc_ptr_data != g.csc_col_ptr.data() || c->csc_row_data != g.csc_row_idx.data() ||
       c->thr != plan.cta_row_threshold) {
     auto fresh = std::make_shared<DeviceGraphCache>();
     GFH_CALL(gf_graph_create(g.num_nodes, g.num_edges, g.csr_row_ptr.data(),
@@ -83,6 +94,8 @@ gf_graph_t device_graph(const Graph& g, const FusionPlan& plan) {
     fresh->e = g.num_edges;
     fresh->row_data = g.csr_row_ptr.data();
     fresh->col_data = g.csr_col_idx.data();
+    fresh->csc_ptr_data = g.csc_col_ptr.data();
+    fresh->csc_row_data = g.csc_row_idx.data();
     fresh->thr = plan.cta_row_threshold;
     c = std::move(fresh);
   }
@@ -116,10 +129,17 @@ void validate_inputs(const Graph& g, const DenseMatrix<T>& Q, const DenseMatrix<
     throw KernelError("engine: Q/K dimension mismatch");
   if (kind.variant == SddmmVariant::Add && (Q.cols != 1 || K.cols != 1))
     throw KernelError("engine: add-SDDMM expects N x 1 el/er");
-  if (kind.variant == SddmmVariant::Dot && Q.cols != V.cols)
-    throw KernelError("engine: B200 fused path requires Q/K width == V width");
   if (kind.variant == SddmmVariant::Add && (Q.rows != g.num_nodes || K.rows != g.num_nodes))
     throw KernelError("engine: el/er must have N rows");
+}
+
+/// Dot attention whose Q/K width differs from V's (the reference allows it,
+/// engine.hpp:239-243): the fused kernels take one head width, so these run
+/// the device's unfused single-step schedule (SDDMM -> softmax -> SpMM; the
+/// 5-launch unfused backward) instead.
+template <typename T>
+bool split_width(const DenseMatrix<T>& Q, const DenseMatrix<T>& V, const SddmmKind& kind) {
+  return kind.variant == SddmmVariant::Dot && Q.cols != V.cols;
 }
 
 int strategy_code(Strategy s) {
@@ -142,6 +162,24 @@ void device_forward(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>
   const gf_attn_desc desc = make_desc<T>(kind, d);
   DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), dv = DevBuf::from(V.data);
   O.assign(static_cast<size_t>(g.num_nodes * d), T(0));
+  if (split_width(Q, V, kind)) {  // unfused device schedule over two head widths
+    lse.clear();  // no softmax records: the backward takes the unfused schedule too
+    const gf_attn_desc qd = make_desc<T>(kind, Q.cols);
+    const size_t eb = sizeof(T) * static_cast<size_t>(std::max<EdgeId>(g.num_edges, 1));
+    DevBuf ds(eb), dp(eb), dO(sizeof(T) * std::max<size_t>(O.size(), 1));
+    if (g.num_edges > 0 && Q.cols > 0) GFH_CALL(gf_sddmm(dg, &qd, dq.p, dk.p, ds.p, nullptr));
+    else GFH_CALL(gf_memset(ds.p, 0, eb, nullptr));
+    GFH_CALL(gf_edge_softmax(dg, desc.dtype, 1, ds.p, dp.p, nullptr));
+    if (d > 0)
+      GFH_CALL(gf_spmm(dg, desc.dtype, 1, static_cast<std::int32_t>(d), dp.p, dv.p, dO.p, nullptr));
+    GFH_CALL(gf_stream_sync(nullptr));
+    if (d > 0) dO.to(O);
+    if (P) {
+      P->assign(static_cast<size_t>(g.num_edges), T(0));
+      dp.to(*P);
+    }
+    return;
+  }
   lse.assign(static_cast<size_t>(4 * g.num_nodes), T(0));  // softmax records (4 per row)
   DevBuf dO(sizeof(T) * O.size()), dl(sizeof(T) * lse.size());
   DevBuf dp(P ? sizeof(T) * static_cast<size_t>(g.num_edges) : 0);
@@ -231,12 +269,17 @@ ExecCounters backward_counters(const Graph& g, std::int64_t d, std::uint64_t b,
 }
 
 template <typename T>
+GradBundle<T> backward_values(const Graph& g, const ForwardContext<T>& ctx,
+                              const DenseMatrix<T>& dO);
+
+template <typename T>
 GradBundle<T> device_backward(const Graph& g, const ForwardContext<T>& ctx,
                               const DenseMatrix<T>& dO) {
   const auto& V = ctx.V;
   if (dO.rows != g.num_nodes || dO.cols != V.cols)
     throw KernelError("spmm_backward: dO shape mismatch");
   validate_inputs(g, ctx.Q, ctx.K, V, ctx.kind);
+  if (split_width(ctx.Q, V, ctx.kind)) return backward_values(g, ctx, dO);
   const std::int64_t d = V.cols;
   const FusionPlan& plan = ctx.plan;
   std::vector<T> O = ctx.O, lse = ctx.lse;
@@ -315,7 +358,9 @@ GradBundle<T> backward_values(const Graph& g, const ForwardContext<T>& ctx,
   gb.dS = EdgeScalars<T>(E);
   if (g.num_nodes == 0 || d == 0) return gb;
   gf_graph_t dg = device_graph(g, ctx.plan);
-  const gf_attn_desc desc = make_desc<T>(ctx.kind, d);
+  // sddmm_backward works on the Q/K width (== d except for split widths)
+  const gf_attn_desc desc =
+      make_desc<T>(ctx.kind, ctx.kind.variant == SddmmVariant::Dot ? ctx.Q.cols : d);
   DevBuf dq = DevBuf::from(ctx.Q.data), dk = DevBuf::from(ctx.K.data), dv = DevBuf::from(V.data),
          dp = DevBuf::from(P), ddo = DevBuf::from(dO.data);
   DevBuf gdp(sizeof(T) * std::max<std::int64_t>(E, 1)), gds(sizeof(T) * std::max<std::int64_t>(E, 1));
@@ -404,6 +449,37 @@ EdgeScalars<T> edge_softmax(const Graph& g, const EdgeScalars<T>& s) {
   GFH_CALL(gf_stream_sync(nullptr));
   dp.to(p.values);
   return p;
+}
+
+template <typename T>
+std::pair<DenseMatrix<T>, DenseMatrix<T>> dense_oracle_forward(const Graph& g,
+                                                               const DenseMatrix<T>& Q,
+                                                               const DenseMatrix<T>& K,
+                                                               const DenseMatrix<T>& V,
+                                                               const SddmmKind& kind) {
+  if (g.num_nodes > 4096) throw KernelError("dense_oracle_forward: N > 4096");
+  const NodeId n = g.num_nodes;
+  const std::int64_t qk = kind.variant == SddmmVariant::Dot ? Q.cols : 1;
+  if (Q.rows != n || K.rows != n || V.rows != n || K.cols != Q.cols ||
+      (kind.variant == SddmmVariant::Add && Q.cols != 1))
+    throw KernelError("dense_oracle_forward: dimension mismatch");
+  DenseMatrix<T> S(n, n), O(n, V.cols);
+  if (n == 0) return {std::move(S), std::move(O)};
+  detail::need_device();
+  gf_attn_desc d = detail::step_desc<T>(kind.variant, qk, kind.scale, kind.leaky_slope,
+                                        kind.variant == SddmmVariant::Dot &&
+                                            kind.l2_normalize_inputs);
+  detail::DevBuf src = detail::DevBuf::from(g.coo_src), dst = detail::DevBuf::from(g.coo_dst),
+                 dq = detail::DevBuf::from(Q.data), dk = detail::DevBuf::from(K.data),
+                 dv = detail::DevBuf::from(V.data), ds(sizeof(T) * S.data.size()),
+                 dO(sizeof(T) * std::max<size_t>(O.data.size(), 1));
+  GFH_CALL(gf_dense_oracle_forward(n, g.num_edges, static_cast<const std::int64_t*>(src.p),
+                                   static_cast<const std::int64_t*>(dst.p), &d, V.cols, dq.p,
+                                   dk.p, dv.p, ds.p, dO.p, nullptr));
+  GFH_CALL(gf_stream_sync(nullptr));
+  ds.to(S.data);
+  dO.to(O.data);
+  return {std::move(S), std::move(O)};
 }
 
 template <typename T>
@@ -713,6 +789,9 @@ PipelineInputs<T> make_pipeline_inputs(const Graph& g, const ConvSpec& spec, std
   template DenseMatrix<T> spmm<T>(const Graph&, const EdgeScalars<T>&, const DenseMatrix<T>&);   \
   template EdgeScalars<T> sddmm<T>(const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&,   \
                                    const SddmmKind&);                                            \
+  template std::pair<DenseMatrix<T>, DenseMatrix<T>> dense_oracle_forward<T>(                    \
+      const Graph&, const DenseMatrix<T>&, const DenseMatrix<T>&, const DenseMatrix<T>&,         \
+      const SddmmKind&);                                                                         \
   template std::pair<EdgeScalars<T>, DenseMatrix<T>> spmm_backward<T>(                           \
       const Graph&, const EdgeScalars<T>&, const DenseMatrix<T>&, const DenseMatrix<T>&);        \
   template EdgeScalars<T> softmax_backward<T>(const Graph&, const EdgeScalars<T>&,               \

@@ -8,6 +8,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# the reference's own python tests, staged by tests/cpp/build_reftests.py, run
+# in their own process through the `graphfuse` alias (test_reference_suites.py)
+collect_ignore_glob = ["cpp/_reftests/*", "alias/*"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")

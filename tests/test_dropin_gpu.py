@@ -193,3 +193,78 @@ def test_run_benchmark_json(cuda, name):
     assert dl[0] == CSV_HEADER + ",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization"
     assert all(float(r.split(",")[12]) > 0 for r in dl[1:])
     assert "| mode |" in md
+
+
+@pytest.mark.parametrize("l2", [False, True])
+def test_qk_width_differs_from_v(cuda, l2):
+    """Dot attention with Q/K width != V width (allowed by the reference,
+    engine.hpp:239-243): forward == the dense numpy reference, and the
+    backward (the device's unfused schedule) == central differences of the
+    device forward."""
+    g = gf.gen_random(30, 3.0, 4)
+    rng = np.random.default_rng(9)
+    Q, K, V = rng.standard_normal((30, 3)), rng.standard_normal((30, 3)), rng.standard_normal((30, 5))
+    if not l2:
+        O, P, _ = gf.forward(g, Q, K, V, scale=0.7)
+        np.testing.assert_allclose(O, dense_reference(g, Q, K, V, scale=0.7), rtol=1e-10,
+                                   atol=1e-12)
+    W = rng.standard_normal((30, 5))
+    dQ, dK, dV, _ = gf.backward(g, Q, K, V, W, scale=0.7, l2_normalize=l2)
+    loss = lambda q, k, v: float(np.sum(gf.forward(g, q, k, v, scale=0.7, l2_normalize=l2)[0] * W))  # noqa: E731
+    h = 1e-6
+    for X, dX, which in ((Q, dQ, 0), (K, dK, 1), (V, dV, 2)):
+        for i, j in ((0, 0), (7, 1), (29, X.shape[1] - 1)):
+            args = [Q.copy(), K.copy(), V.copy()]
+            args[which][i, j] += h
+            up = loss(*args)
+            args[which][i, j] -= 2 * h
+            dn = loss(*args)
+            assert dX[i, j] == pytest.approx((up - dn) / (2 * h), rel=1e-5, abs=1e-7)
+
+
+def test_dense_oracle_forward_matches_sparse(cuda):
+    """dense_oracle_forward (kernels.hpp:122-166) is a device op of the
+    drop-in (gf_dense_oracle_forward); the C++ reference suites call it
+    directly (test_reference_suites.py); here through the C-ABI it matches
+    the reference oracle on a GT, AGNN and GAT case."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2411_16127_b200._capi import AttnDesc, check, lib
+
+    n = 64
+    g = oracle.from_coo(n, *np.nonzero(np.random.default_rng(3).random((n, n)) < 0.1)[::-1])
+    src = torch.from_numpy(np.ascontiguousarray(g.col)).cuda()
+    dst = torch.from_numpy(np.repeat(np.arange(n), np.diff(g.row_ptr))).cuda()
+    rng = np.random.default_rng(1)
+    for variant, l2, w in ((0, 0, 4), (0, 1, 4), (1, 0, 1)):
+        Q, K, V = rng.standard_normal((n, w)), rng.standard_normal((n, w)), rng.standard_normal((n, 3))
+        d = AttnDesc(dtype=1, variant=variant, l2=l2, heads=1, head_dim=w, scale=0.5, slope=0.2)
+        tq, tk, tv = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+        S = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+        O = torch.zeros(n, 3, dtype=torch.float64, device="cuda")
+        check(lib().gf_dense_oracle_forward(n, g.e, C.c_void_p(src.data_ptr()),
+                                            C.c_void_p(dst.data_ptr()), C.byref(d), 3,
+                                            C.c_void_p(tq.data_ptr()), C.c_void_p(tk.data_ptr()),
+                                            C.c_void_p(tv.data_ptr()), C.c_void_p(S.data_ptr()),
+                                            C.c_void_p(O.data_ptr()), None), "dense oracle")
+        torch.cuda.synchronize()
+        # reference dense oracle arithmetic restated in numpy
+        if l2:
+            Qe = Q / np.maximum(np.linalg.norm(Q, axis=1, keepdims=True), 1e-12)
+            Ke = K / np.maximum(np.linalg.norm(K, axis=1, keepdims=True), 1e-12)
+        else:
+            Qe, Ke = Q, K
+        s = (0.5 * np.einsum("ij,ij->i", Qe[g.col], Ke[dst.cpu().numpy()]) if not variant else
+             np.where((x := Q[g.col, 0] + K[dst.cpu().numpy(), 0]) >= 0, x, 0.2 * x))
+        Sd = np.zeros((n, n))
+        Sd[dst.cpu().numpy(), g.col] = s
+        np.testing.assert_allclose(S.cpu().numpy(), Sd, rtol=1e-12, atol=1e-14)
+        Ow = np.zeros((n, 3))
+        for v in range(n):
+            b, e = g.row_ptr[v], g.row_ptr[v + 1]
+            if e > b:
+                p = np.exp(s[b:e] - s[b:e].max())
+                Ow[v] = (p / p.sum()) @ V[g.col[b:e]]
+        np.testing.assert_allclose(O.cpu().numpy(), Ow, rtol=1e-12, atol=1e-13)
