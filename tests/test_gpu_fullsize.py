@@ -11,6 +11,10 @@ graph in a test) plus oracle parity on sampled rows:
 * transposed aggregation (pass B): sum_u dV[u] = sum over non-empty rows v of
   dO[v] (each row's probabilities sum to 1), and for GAT sum_u del[u] =
   sum_v der[v] (both are sum_e dS_e lrelu'(pre_e));
+* sampled COLUMNS (incl. the largest out-hub) == the oracle on the complete
+  in-edge sets of every destination they reach, so pass B's source-owned
+  gradients dV and dQ|del are checked elementwise (autograd.hpp:33-58,
+  120-154: dV and dQ over CSC);
 * linearity in dO: gradients of 2 dO are exactly 2x (power-of-two scaling);
 * determinism: a repeated step is bitwise identical.
 Tolerance for fp32 sums over 10^8 terms: relative 1e-4 of the summed
@@ -25,6 +29,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = {
     "c4": ("reddit", "add", 8, 8),
+    "c5gat": ("products", "add", 8, 8),
     "c5gt": ("products", "dot", 8, 16),
 }
 
@@ -54,6 +59,21 @@ def _setup(name):
     u = lambda *s, a=1.0: (torch.rand(*s, device=dev, generator=g) * 2 - 1) * a  # noqa: E731
     Q, K, V, dO = u(n, qk, a=amp), u(n, qk, a=amp), u(n, H * D), u(n, H * D)
     return n, rp, col, dg, spec, Q, K, V, dO
+
+
+def _sub_rows(n, rp_h, col_h, rows):
+    """oracle.CSR of the complete in-edge sets of `rows` (other rows empty)."""
+    segs = [col_h[rp_h[v]: rp_h[v + 1]] for v in rows]
+    counts = np.zeros(n, np.int64)
+    counts[rows] = [len(s) for s in segs]
+    sub_ptr = np.zeros(n + 1, np.int64)
+    sub_ptr[1:] = np.cumsum(counts)
+    sub_col = np.concatenate(segs) if segs else np.zeros(0, np.int64)
+    dst = np.repeat(rows, [len(s) for s in segs])
+    order = np.argsort(sub_col, kind="stable")
+    csc_ptr = np.zeros(n + 1, np.int64)
+    csc_ptr[1:] = np.cumsum(np.bincount(sub_col, minlength=n))
+    return oracle.CSR(n, sub_ptr, sub_col, csc_ptr, dst[order], order.astype(np.int64))
 
 
 def _step(dg, spec, Q, K, V, dO):
@@ -106,20 +126,29 @@ def test_fullsize_properties(cuda, name):
     rows = np.unique(np.concatenate([[int(torch.argmax(deg))],
                                      rng.choice(n, 300, replace=False)]))
     rp_h, col_h = rp.cpu().numpy().astype(np.int64), col.cpu().numpy().astype(np.int64)
-    sub_ptr = np.zeros(n + 1, np.int64)
-    segs = [col_h[rp_h[v]: rp_h[v + 1]] for v in rows]
-    counts = np.zeros(n, np.int64)
-    counts[rows] = [len(s) for s in segs]
-    sub_ptr[1:] = np.cumsum(counts)
-    sub_col = np.concatenate(segs) if segs else np.zeros(0, np.int64)
-    dst = np.repeat(rows, [len(s) for s in segs])
-    order = np.argsort(sub_col, kind="stable")
-    csc_ptr = np.zeros(n + 1, np.int64)
-    csc_ptr[1:] = np.cumsum(np.bincount(sub_col, minlength=n))
-    sub = oracle.CSR(n, sub_ptr, sub_col, csc_ptr, dst[order], order.astype(np.int64))
+    sub = _sub_rows(n, rp_h, col_h, rows)
     hQ, hK, hV, hdO = (x.cpu().numpy() for x in (Q, K, V, dO))
     O_ref = oracle.forward(sub, hQ, hK, hV, H, D, spec.variant, False, spec.scale, 0.2)
     _, dK_ref, _ = oracle.backward(sub, hQ, hK, hV, hdO, H, D, spec.variant, False, spec.scale, 0.2)
     got_O, got_dK = O.cpu().numpy()[rows], dK.cpu().numpy()[rows]
     assert rel_err(got_O, O_ref[rows]) <= 1e-4
     assert rel_err(got_dK, dK_ref[rows]) <= 1e-4
+    del sub, O_ref, dK_ref
+
+    # sampled columns (pass B, source-owned): every out-edge u -> v of a
+    # sampled u lands in a complete row v of the sub-graph, so the oracle's
+    # dV[u] and dQ|del[u] there equal the full graph's
+    out_deg = np.bincount(col_h, minlength=n)
+    k = 40 if name == "c4" else 300  # C4 rows reached are hub-heavy (~670 in-edges each)
+    cols = np.unique(np.concatenate([[int(np.argmax(out_deg))],
+                                     rng.choice(n, k, replace=False)]))
+    is_col = np.zeros(n, bool)
+    is_col[cols] = True
+    dst_all = np.repeat(np.arange(n), np.diff(rp_h))
+    reach = np.unique(dst_all[is_col[col_h]])
+    del dst_all
+    sub = _sub_rows(n, rp_h, col_h, reach)
+    dQ_ref, _, dV_ref = oracle.backward(sub, hQ, hK, hV, hdO, H, D, spec.variant, False,
+                                        spec.scale, 0.2)
+    assert rel_err(dV.cpu().numpy()[cols], dV_ref[cols]) <= 1e-4
+    assert rel_err(dQ.cpu().numpy()[cols], dQ_ref[cols]) <= 1e-4

@@ -318,3 +318,81 @@ def test_bad_arguments_fail_loudly(cuda):
         fused.attn_forward(dg, fused.AttnSpec("add", 1, 8, l2=True), x, x, x)
     with pytest.raises(GFError, match="null operand"):
         fused.attn_forward(dg, fused.AttnSpec("dot", 1, 8), None, x, x)
+
+
+# --------------------------------------------------------------- bench graphs --
+def _bench_graph(name):
+    import os
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    n, src, dst = bench.gen_graph_device(name, torch.device("cuda"))
+    return oracle.from_coo(n, src.cpu().numpy(), dst.cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg", [("molhiv", "dot", False, 8, 16), ("pubmed", "dot", True, 1, 128),
+                                 ("pubmed", "dot", True, 8, 16), ("cora", "add", False, 8, 8)],
+                         ids=["C2-GT-8x16", "C3-AGNN-1x128", "C3-AGNN-8x16", "C1-GAT-8x8"])
+def test_bench_graph_parity(cuda, cfg):
+    """The exact graphs bench.py times for C1-C3 (device generators), whole
+    graph, every output and gradient vs the oracle."""
+    graph, variant, l2, H, D = cfg
+    g = _bench_graph(graph)
+    check_against_oracle(g, variant, l2, H, D, np.float32,
+                         scale=(1.0 / np.sqrt(D)) if not l2 else 1.0)
+
+
+def _symmetric_power_law(n, mx, seed=3):
+    """Power-law in-degrees made undirected (every edge both ways), like the
+    real Reddit / products graphs: the in-hubs are also out-hubs, so pass B's
+    CTA-column path meets super columns."""
+    from paper_2411_16127_b200 import fused
+
+    s, d = fused.gen_power_law_device(n, mx, 0.34, seed=seed)
+    s, d = s.cpu().numpy(), d.cpu().numpy()
+    key = np.unique(np.concatenate([d * n + s, s * n + d]))
+    return oracle.from_coo(n, key % n, key // n)
+
+
+@pytest.mark.parametrize("cfg", [("add", False, 8, 8), ("dot", False, 8, 16), ("dot", True, 1, 128)],
+                         ids=["GAT", "GT", "AGNN"])
+@pytest.mark.parametrize("thr", [0, 256])
+def test_symmetric_hubs_parity(cuda, cfg, thr):
+    variant, l2, H, D = cfg
+    g = _symmetric_power_law(6_000, 2_600)
+    out_deg = np.diff(g.csc_ptr)
+    assert out_deg.max() >= 1_500 and np.diff(g.row_ptr).max() >= 1_500
+    check_against_oracle(g, variant, l2, H, D, np.float32, cta_threshold=thr,
+                         scale=(1.0 / np.sqrt(D)) if not l2 else 1.0)
+
+
+def test_device_from_coo_bit_exact_c4_scale(cuda):
+    """Device from_coo on the 114 M-edge C4 graph (the bench's own input,
+    shuffled) == the oracle's from_coo, all five arrays bit for bit."""
+    import os
+    import sys
+
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    n, src, dst = bench.gen_graph_device("reddit", torch.device("cuda"))
+    perm = torch.randperm(src.numel(), device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    src, dst = src[perm], dst[perm]
+    del perm
+    out = fused.from_coo_device(n, src, dst)
+    hs, hd = src.cpu().numpy(), dst.cpu().numpy()
+    del src, dst
+    ref = oracle.from_coo(n, hs, hd)
+    del hs, hd
+    assert ref.e > 100_000_000
+    for name, a, b in zip(("row_ptr", "col", "csc_ptr", "csc_row", "csc_perm"), out,
+                          (ref.row_ptr, ref.col, ref.csc_ptr, ref.csc_row, ref.csc_perm)):
+        assert np.array_equal(a.cpu().numpy(), b), name
