@@ -76,3 +76,71 @@ extern "C" int gf_measure_l2_gather(size_t footprint_bytes, int32_t row_bytes, i
   cudaFree(sink);
   return rc;
 }
+
+// Scatter-reduction probe (design measurement, not on the product path): per
+// CSC edge u -> v, 8 lanes add one fp32 per head into table[v][0..7] (the
+// shape of a GAT der[v] update issued from a source-owned pass), as scalar
+// red.add.f32 (mode 0), red.add.v4.f32 from 2 lanes (mode 1), plain stores
+// (mode 2) or 32 B gathers (mode 3).  Warp per column, 4 edges per step.
+namespace gfb {
+namespace {
+__global__ void __launch_bounds__(256) scatter_probe(int n, const int32_t* __restrict__ ptr,
+                                                     const int32_t* __restrict__ idx,
+                                                     float* __restrict__ table, int mode,
+                                                     float* __restrict__ sink) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3, h = lane & 7;
+  float acc = 0.f;
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += (gridDim.x * blockDim.x) >> 5) {
+    const int b = __ldg(ptr + u), e = __ldg(ptr + u + 1);
+    for (int j = b + sub; j < e; j += 4) {
+      const int v = ld_idx(idx + j);
+      float* p = table + static_cast<size_t>(v) * 8;
+      const float x = 1e-3f * (h + 1);
+      if (mode == 0) {
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p + h), "f"(x) : "memory");
+      } else if (mode == 1) {
+        if ((h & 3) == 0)
+          asm volatile("red.global.add.v4.f32 [%0], {%1,%1,%1,%1};" ::"l"(p + h), "f"(x) : "memory");
+      } else if (mode == 4) {
+        unsigned long long* q = reinterpret_cast<unsigned long long*>(table) + static_cast<size_t>(v) * 8;
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(q + h), "l"(static_cast<unsigned long long>(h + 1)) : "memory");
+      } else if (mode == 2) {
+        p[h] = x;
+      } else {
+        acc += __ldg(p + h);
+      }
+    }
+  }
+  if (acc == 12345.678f) sink[threadIdx.x] = acc;
+}
+}  // namespace
+}  // namespace gfb
+
+extern "C" int gf_probe_scatter(int64_t n, const int32_t* csc_ptr, const int32_t* csc_row,
+                                float* table, int32_t mode, int32_t iters, float* ms_out,
+                                void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  float* sink = nullptr;
+  GF_CHECK_CUDA(cudaMalloc(&sink, sizeof(float) * 256));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = 148 * 8;
+  gfb::scatter_probe<<<blocks, 256, 0, s>>>(static_cast<int>(n), csc_ptr, csc_row, table, mode, sink);
+  cudaEventRecord(a, s);
+  for (int i = 0; i < iters; ++i)
+    gfb::scatter_probe<<<blocks, 256, 0, s>>>(static_cast<int>(n), csc_ptr, csc_row, table, mode,
+                                              sink);
+  cudaEventRecord(b, s);
+  int rc = cudaEventSynchronize(b) == cudaSuccess ? GF_OK : GF_ERR_CUDA;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *ms_out = ms / iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (rc) gfb::set_error("gf_probe_scatter: kernel failed");
+  return rc;
+}
