@@ -222,6 +222,7 @@ static void ensure_l2_setaside() {
 
 extern "C" int gf_l2_persist(size_t bytes) {
   int dev = 0, max_persist = 0;
+  GF_CHECK_CUDA(cudaFree(nullptr));  // the context calls below need a current context
   GF_CHECK_CUDA(cudaGetDevice(&dev));
   GF_CHECK_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
   if (bytes == 0) GF_CHECK_CUDA(cudaCtxResetPersistingL2Cache());
@@ -240,6 +241,7 @@ extern "C" int gf_l2_persist_get(size_t* bytes) {
 }
 
 extern "C" int gf_l2_reset_persisting(void) {
+  GF_CHECK_CUDA(cudaFree(nullptr));
   GF_CHECK_CUDA(cudaCtxResetPersistingL2Cache());
   return GF_OK;
 }
