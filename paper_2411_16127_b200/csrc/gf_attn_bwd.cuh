@@ -818,7 +818,7 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   const bool dot = variant == GF_DOT;
   // Each pass picks the fast path independently (both paths use the same
   // record layout), so a misaligned operand of one pass never affects the other.
-  const FastShape fs = fast_shape(a.H, a.D, sizeof(T));
+  const FastShape fs = fast_shape(a.H, a.D, sizeof(T), g.e);
   const int cb = fs.cb;
   const bool base = fs.ok && static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31) &&
                     aligned(a.stats, 32);

@@ -23,6 +23,7 @@
 // / softmax work is done once per edge, not once per 16 B chunk; 32/LPE edges
 // per warp step, unrolled U deep.  Nothing of size E x H is written: outputs
 // are O (N x F) and the per-(row, head) softmax records (gf_device.cuh Rec).
+#include <cstdlib>
 #include <type_traits>
 
 #include "gf_device.cuh"
@@ -514,7 +515,11 @@ int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cuda
 }  // namespace
 
 #ifdef GF_FWD_PRIMARY  // non-template definitions: emitted by the f32 unit only
-FastShape fast_shape(int H, int D, int elem_bytes) {
+FastShape fast_shape(int H, int D, int elem_bytes, int64_t edges) {
+  static const int force_cpl = [] {
+    const char* e = std::getenv("GF_CPL");
+    return e && *e ? std::atoi(e) : 0;
+  }();
   FastShape f;
   if (H < 1 || D < 1) return f;
   const long row = static_cast<long>(D) * elem_bytes;
@@ -522,7 +527,9 @@ FastShape fast_shape(int H, int D, int elem_bytes) {
   if (!cb) return f;
   const long cph = row / cb;
   auto pow2 = [](long x) { return x > 0 && (x & (x - 1)) == 0; };
-  const int cpl = cph >= 2 ? 2 : 1;
+  int cpl = cph >= 2 ? 2 : 1;
+  if (cpl == 2 && cb == 32 && static_cast<long>(H) * cph <= 32 && force_cpl == 1) cpl = 1;
+  (void)edges;
   if (cb == 16 && cpl != 1) return f;  // 16 B chunks only for one-chunk heads
   const long lph = cph / cpl;
   const long lpe = static_cast<long>(H) * lph;
@@ -562,7 +569,7 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
   if (g.n == 0) return GF_OK;
   FwdArgs<T> a = a0;
   if (a.n == 0) return GF_OK;  // every row skipped (row-sharded graph)
-  const FastShape fs = fast_shape(a.H, a.D, sizeof(T));
+  const FastShape fs = fast_shape(a.H, a.D, sizeof(T), a.e);
   const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
   const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
                   aligned(a.stats, 32) &&

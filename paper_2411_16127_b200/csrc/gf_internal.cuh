@@ -34,11 +34,12 @@ void set_error(const std::string& msg);
   } while (0)
 
 // ----------------------------------------------------------------- scratch --
-// Stream-ordered scratch (cudaMallocAsync) from the device's default pool.
-// The first call raises the pool's release threshold (8 GiB) so freed
-// scratch stays mapped across synchronisations: with the default threshold
-// of 0 every sync hands it back to the driver and the next call pays for a
-// fresh physical mapping (measured: +5.6 ms per unfused AGNN backward on C3).
+// Stream-ordered scratch (cudaMallocFromPoolAsync) from a library-private
+// memory pool per device whose release threshold (8 GiB) keeps freed scratch
+// mapped across synchronisations: with a threshold of 0 every sync hands it
+// back to the driver and the next call pays for a fresh physical mapping
+// (measured: +5.6 ms per unfused AGNN backward on C3).  The device's default
+// pool (the host application's) is untouched; gf_scratch_trim() releases.
 cudaError_t scratch_alloc_raw(void** p, size_t bytes, cudaStream_t s);
 template <class P>
 inline cudaError_t scratch_alloc(P** p, size_t bytes, cudaStream_t s) {
@@ -237,7 +238,11 @@ struct FastShape {
   bool ok = false;
   int cb = 0, lpe = 0, cpl = 0, lph = 0;
 };
-FastShape fast_shape(int H, int D, int elem_bytes);
+// Heads of >= 2 chunks take two chunks per lane.  One chunk per lane (twice
+// the lanes per edge, fewer registers) measured slower on every config, small
+// graphs included (C2 0.71 -> 0.45, C3 0.94 -> 0.67, C5 GT 1.78 -> 1.17
+// GEdges/s, profiles/r2/ab_r2_one_chunk_lanes.txt); GF_CPL=1 forces it (A/B).
+FastShape fast_shape(int H, int D, int elem_bytes, int64_t edges);
 
 }  // namespace gfb
 
