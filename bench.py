@@ -1393,6 +1393,32 @@ def run_ours(args, cfg, rank, world, full=True):
             cpu = {"value": None, "unit": "GEdges/s", "cores": os.cpu_count(),
                    "kind": "reference", "sample": f"failed: {ex}"}
 
+    # Measured per-launch traffic of each kernel, live (CUPTI range profiler
+    # through gf_measure_metrics; cold L2 before the launch, like ncu's
+    # per-kernel cache control): DRAM bytes, and L2 -> L1 bytes next to the
+    # algorithmic bytes (the L2-gather bound's evidence).
+    measured = None
+    if full:
+        from paper_2411_16127_b200._capi import GFError
+
+        mets = ["dram__bytes_read.sum", "dram__bytes_write.sum",
+                "l1tex__m_xbar2l1tex_read_bytes.sum"]
+        runs = {"fwd": lambda: fused.attn_forward(dg, spec, Q, K, V, O=O, stats=stats, stream=stream),
+                "bwd_rows": lambda: fused.attn_backward_rows(dg, spec, Q, K, V, O, stats, dO, dK,
+                                                             stream=stream),
+                "bwd_cols": lambda: fused.attn_backward_cols(dg, spec, Q, K, V, stats, dO, dQ, dV,
+                                                             stream=stream)}
+        try:
+            measured = {}
+            for k, fn in runs.items():
+                m = fused.measure_metrics(fn, mets, prep=lambda: cold_l2(flush))
+                measured[k] = {"dram_bytes": m[mets[0]] + m[mets[1]],
+                               "l2_to_l1_bytes": m[mets[2]],
+                               "algorithmic_bytes": algorithmic_bytes(k, layer, nb, e_of[k], H, D)}
+        except GFError as ex:  # no CUPTI / permission: the committed ncu file stands
+            measured = {"error": str(ex)[:200]}
+        if "error" not in measured:
+            traffic = measured[dom]["dram_bytes"]
     tables_fit = tables_bytes <= L2_BYTES
     hbm_roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -1422,6 +1448,10 @@ def run_ours(args, cfg, rank, world, full=True):
                       "parallelism": (f"row-sharded x{world} (NCCL all-gather)" if sharded
                                       else "1 GPU")},
             "l2_carveout": carve,
+            "measured_bytes": measured,
+            "measured_bytes_note": ("per launch, cold L2 (persisting lines reset + 256 MiB "
+                                    "flush), CUPTI range profiler via gf_measure_metrics; "
+                                    "roofline.traffic = dram_bytes of the dominant kernel"),
             "kernels_ms": {k: round(v, 4) for k, v in means.items()},
             "preprocess_ms": ({"from_coo": round(pre_coo_ms, 2), "schedule": round(pre_sched_ms, 2),
                                "note": "one-time graph setup on the device, wall clock with syncs: "

@@ -313,6 +313,17 @@ int gf_l2_persist_get(size_t* bytes);
 int gf_l2_reset_persisting(void);
 int gf_scratch_trim(void);
 
+/* ---- measured counters (CUPTI range profiler; libcupti loaded on demand) ----
+ * Runs fn(user) inside one profiled range, once per counter pass (user
+ * replay; byte counters need one), with prep(user) (nullable) before each
+ * pass outside the range, synchronising the device after each; evaluates the
+ * n_metrics (1..16) Nsight-Compute-style metric names (e.g.
+ * "dram__bytes_read.sum", "dram__bytes_write.sum",
+ * "l1tex__m_xbar2l1tex_read_bytes.sum") into values.  GF_ERR_UNSUPPORTED
+ * without libcupti or without profiling permission.  Not for timing runs. */
+int gf_measure_metrics(void (*prep)(void*), void (*fn)(void*), void* user,
+                       const char* const* metrics, int32_t n_metrics, double* values);
+
 /* ---- diagnostics ----
  * Measured gather bandwidth (GB/s) of rows of row_bytes (32..1024, lanes read
  * consecutive 32 B chunks with 256-bit non-coherent loads) chosen in hashed

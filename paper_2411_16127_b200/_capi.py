@@ -85,6 +85,8 @@ SIGNATURES = {
                                           _vp, _vp, C.POINTER(C.c_int64), _vp]),
     "gf_dense_oracle_forward": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, C.POINTER(AttnDesc),
                                           C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gf_measure_metrics": (C.c_int, [C.c_void_p, C.c_void_p, _vp, C.POINTER(C.c_char_p),
+                                     C.c_int32, C.POINTER(C.c_double)]),
     "gf_l2_persist": (C.c_int, [C.c_size_t]),
     "gf_l2_persist_get": (C.c_int, [C.POINTER(C.c_size_t)]),
     "gf_l2_reset_persisting": (C.c_int, []),

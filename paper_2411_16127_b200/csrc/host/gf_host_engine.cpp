@@ -211,6 +211,56 @@ double device_forward_ms(const Graph& g, const FusionPlan& plan, const DenseMatr
                                 reps, &ms, nullptr));
   return ms;
 }
+/// Measured DRAM bytes (read + write, CUPTI range profiler through
+/// gf_measure_metrics) of `mode`'s forward kernels on device-resident inputs,
+/// L2 flushed (256 MiB write) before the profiled range.  Returns -1 when the
+/// counters are unavailable (no libcupti / no profiling permission).
+template <typename T>
+double device_forward_dram_bytes(const Graph& g, const FusionPlan& plan, const DenseMatrix<T>& Q,
+                                 const DenseMatrix<T>& K, const DenseMatrix<T>& V,
+                                 const SddmmKind& kind, Strategy mode) {
+  validate_inputs(g, Q, K, V, kind);
+  struct Region {
+    gf_graph_t dg;
+    gf_attn_desc desc;
+    int strategy;
+    void *q, *k, *v, *o, *l, *flush;
+    size_t flush_bytes;
+  };
+  DevBuf dq = DevBuf::from(Q.data), dk = DevBuf::from(K.data), dv = DevBuf::from(V.data);
+  DevBuf dO(sizeof(T) * static_cast<size_t>(std::max<std::int64_t>(1, g.num_nodes * V.cols))),
+      dl(sizeof(T) * static_cast<size_t>(std::max<std::int64_t>(1, 4 * g.num_nodes)));
+  const size_t fb = size_t(256) << 20;
+  DevBuf flush(fb);
+  Region r{device_graph(g, plan), make_desc<T>(kind, V.cols), strategy_code(mode), dq.p, dk.p,
+           dv.p, dO.p, dl.p, flush.p, fb};
+  auto prep = [](void* u) {
+    auto* x = static_cast<Region*>(u);
+    gf_l2_reset_persisting();
+    gf_memset(x->flush, 0, x->flush_bytes, nullptr);
+  };
+  auto run = [](void* u) {
+    auto* x = static_cast<Region*>(u);
+    gf_attn_fwd_strategy(x->dg, &x->desc, x->strategy, x->q, x->k, x->v, x->o, x->l, nullptr,
+                         nullptr, 0, nullptr);
+  };
+  const char* names[2] = {"dram__bytes_read.sum", "dram__bytes_write.sum"};
+  double vals[2] = {0, 0};
+  const int rc = gf_measure_metrics(prep, run, &r, names, 2, vals);
+  if (rc == GF_ERR_UNSUPPORTED) return -1.0;
+  if (rc != GF_OK) device_fail("gf_measure_metrics");
+  return vals[0] + vals[1];
+}
+template double device_forward_dram_bytes<float>(const Graph&, const FusionPlan&,
+                                                 const DenseMatrix<float>&,
+                                                 const DenseMatrix<float>&,
+                                                 const DenseMatrix<float>&, const SddmmKind&,
+                                                 Strategy);
+template double device_forward_dram_bytes<double>(const Graph&, const FusionPlan&,
+                                                  const DenseMatrix<double>&,
+                                                  const DenseMatrix<double>&,
+                                                  const DenseMatrix<double>&, const SddmmKind&,
+                                                  Strategy);
 template double device_forward_ms<float>(const Graph&, const FusionPlan&, const DenseMatrix<float>&,
                                          const DenseMatrix<float>&, const DenseMatrix<float>&,
                                          const SddmmKind&, Strategy, int);

@@ -416,3 +416,20 @@ def gen_molecules_device(mols, atoms, rings, seed=0, device="cuda", stream=None)
     check(lib().gf_gen_molecules_device(mols, atoms, rings, seed, cap, _p(src), _p(dst),
                                         C.byref(out), _stream(stream)), "gf_gen_molecules_device")
     return src[: out.value], dst[: out.value]
+
+
+_REGION_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+
+def measure_metrics(fn, metrics, prep=None):
+    """Hardware counters of the kernels `fn()` launches (gf_measure_metrics:
+    CUPTI range profiler, one range, user replay; `prep()` runs before every
+    pass outside the range, e.g. an L2 flush).  Returns {metric: value}.
+    Raises GFError (status GF_ERR_UNSUPPORTED = 4) without CUPTI / permission."""
+    cb = _REGION_FN(lambda _u: fn())
+    pcb = _REGION_FN(lambda _u: prep()) if prep is not None else None
+    names = (C.c_char_p * len(metrics))(*[m.encode() for m in metrics])
+    vals = (C.c_double * len(metrics))()
+    check(lib().gf_measure_metrics(C.cast(pcb, C.c_void_p) if pcb else None, C.cast(cb, C.c_void_p),
+                                   None, names, len(metrics), vals), "gf_measure_metrics")
+    return {m: float(v) for m, v in zip(metrics, vals)}

@@ -190,8 +190,12 @@ def test_run_benchmark_json(cuda, name):
     assert [strip(a) for a in lines[1:]] == [strip(b) for b in again[1:]]
     dcsv, md = _core.run_benchmark_json_device(text)
     dl = dcsv.strip().split("\n")
-    assert dl[0] == CSV_HEADER + ",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization"
+    assert dl[0] == (CSV_HEADER + ",device_ms,device_speedup_vs_unfused,"
+                     "device_bandwidth_utilization,device_dram_bytes")
     assert all(float(r.split(",")[12]) > 0 for r in dl[1:])
+    # measured DRAM bytes of each mode's forward (CUPTI), L2 flushed first: at
+    # least the gathered inputs' footprint is read from DRAM
+    assert all(int(r.split(",")[15]) > 0 for r in dl[1:]), dl
     assert "| mode |" in md
 
 
