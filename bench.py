@@ -503,6 +503,36 @@ def cpu_reference_layer(sub, layer, H, D, e_full, pipe_s, rg=None):
                     "measured projection time and the pipeline time scaled to all edges"}
 
 
+def dropin_api_timing(n, rp, col, csc, H, D, layer, e, reps=1):
+    """gfh_time_api_step (libgraphfuse.so): the unchanged single-head C++ API
+    (engine.hpp:331-336 run_strategy<float>, autograd.hpp:210-226
+    fused_backward<float>) for all H heads with host vectors; ms per step."""
+    import ctypes as C
+
+    import numpy as np
+
+    L = C.CDLL(os.path.join(ROOT, "paper_2411_16127_b200", "libgraphfuse.so"))
+    f = L.gfh_time_api_step
+    f.restype = C.c_int
+    f.argtypes = ([C.c_int64, C.c_int64] + [C.c_void_p] * 5
+                  + [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                     C.POINTER(C.c_double), C.c_char_p, C.c_int])
+    arrs = [np.ascontiguousarray(a, np.int64) for a in (rp, col, csc[0], csc[1], csc[2])]
+    fm, bm = C.c_double(), C.c_double()
+    err = C.create_string_buffer(512)
+    t0 = time.time()
+    rc = f(n, e, *[a.ctypes.data_as(C.c_void_p) for a in arrs], H, D, 1 if layer == "gat" else 0,
+           reps, C.byref(fm), C.byref(bm), err, 512)
+    if rc:
+        return {"error": err.value.decode()[:200]}
+    ms = fm.value + bm.value
+    return {"value": e / (ms / 1e3) / 1e9, "unit": "GEdges/s", "ms_per_step": ms,
+            "fwd_ms": fm.value, "bwd_ms": bm.value, "wall_s": round(time.time() - t0, 1),
+            "note": f"reference-facing C++ API: run_strategy<float> + fused_backward<float> for "
+                    f"each of the {H} heads (single-head API), host buffers: Q/K/V uploaded, O "
+                    "and the E-length P downloaded, counters modelled, context re-uploaded"}
+
+
 def spawn_ranks(args):
     """`bench.py --gpus N` without a launcher: re-run under
     torch.distributed.run with N ranks on this node (127.0.0.1)."""
@@ -535,6 +565,9 @@ def main(argv=None):
                     help="opt-in persisting-L2 set-aside for the evict-last node tables "
                          "(gf_l2_persist); 0 = none.  The line also reports the value without it")
     ap.add_argument("--cta-threshold", type=int, default=0)
+    ap.add_argument("--no-api", action="store_true",
+                    help="skip timing the reference-facing C++ API path (run_strategy + "
+                         "fused_backward per head, host buffers)")
     ap.add_argument("--no-layer", action="store_true",
                     help="skip the layer-level (projection + pipeline) measurement")
     ap.add_argument("--no-ablation", action="store_true",
@@ -1058,7 +1091,7 @@ def run_ours(args, cfg, rank, world, full=True):
     n, src, dst = gen_graph_device(graph, dev)
     torch.cuda.synchronize()
     t_pre = time.perf_counter()
-    row_ptr, col, csc_ptr, csc_row, _ = fused.from_coo_device(n, src, dst)
+    row_ptr, col, csc_ptr, csc_row, csc_perm = fused.from_coo_device(n, src, dst)
     torch.cuda.synchronize()
     pre_coo_ms = (time.perf_counter() - t_pre) * 1e3
     del src, dst
@@ -1096,9 +1129,11 @@ def run_ours(args, cfg, rank, world, full=True):
         pre_sched_ms = (time.perf_counter() - t_pre) * 1e3
         n_tab = n
     need_cpu = full and rank == 0 and not sharded and not args.no_cpu_baseline
-    host_rp = row_ptr.cpu().numpy() if need_cpu else None
-    host_col = col.cpu().numpy() if need_cpu else None
-    del row_ptr, col, csc_ptr, csc_row
+    need_api = full and rank == 0 and not sharded and not args.no_api
+    host_rp = row_ptr.cpu().numpy() if (need_cpu or need_api) else None
+    host_col = col.cpu().numpy() if (need_cpu or need_api) else None
+    host_csc = ([t.cpu().numpy() for t in (csc_ptr, csc_row, csc_perm)] if need_api else None)
+    del row_ptr, col, csc_ptr, csc_row, csc_perm
     O = torch.zeros(n_tab, F, device=dev)
     stats = torch.zeros(n_tab, H, 4, device=dev)
     dQ, dK, dV = (torch.zeros(n_tab, qk, device=dev), torch.zeros(n_tab, qk, device=dev),
@@ -1432,6 +1467,12 @@ def run_ours(args, cfg, rank, world, full=True):
                "why": "the gathered node tables fit L2 (gathered_tables_bytes <= 126 MiB): ncu "
                       "shows DRAM bytes << algorithmic bytes (traffic) while L1<-L2 bytes equal "
                       "them, so the L2 gather rate, not HBM, bounds the kernel"}
+    # The reference-facing C++ operator API itself, timed once: every head
+    # through run_strategy<float> + fused_backward<float> with host buffers
+    # (gf_host_timing.cpp).  What a reference user pays per layer step.
+    api = None
+    if need_api:
+        api = dropin_api_timing(n, host_rp, host_col, host_csc, H, D, layer, e)
     if rank == 0:
         info = dg.info
         out = {
@@ -1448,6 +1489,7 @@ def run_ours(args, cfg, rank, world, full=True):
                       "parallelism": (f"row-sharded x{world} (NCCL all-gather)" if sharded
                                       else "1 GPU")},
             "l2_carveout": carve,
+            "dropin_api": api,
             "measured_bytes": measured,
             "measured_bytes_note": ("per launch, cold L2 (persisting lines reset + 256 MiB "
                                     "flush), CUPTI range profiler via gf_measure_metrics; "

@@ -95,7 +95,9 @@ int gf_device_ok(void);
 
 /* Memory plumbing for hosts that do not link the CUDA runtime themselves
  * (the C++ host layer and the pybind module use only this C-ABI).
- * kind: 0 host->device, 1 device->host, 2 device->device. */
+ * gf_malloc / gf_free are stream-ordered on the legacy default stream (the
+ * library's private pool): use the buffer on that stream or on a blocking
+ * stream.  kind: 0 host->device, 1 device->host, 2 device->device. */
 int gf_malloc(size_t bytes, void** out);
 int gf_free(void* p);
 int gf_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);

@@ -71,6 +71,10 @@ extern "C" int gf_device_ok(void) {
   return p.major == 10 && p.minor == 0;  // built for sm_100a only
 }
 
+// Device buffers of the host API layer come from the library's private
+// stream-ordered pool on the legacy default stream (which orders them against
+// every blocking stream): cudaMalloc / cudaFree per operator call cost
+// milliseconds each (cudaFree synchronises the device) on the drop-in path.
 extern "C" int gf_malloc(size_t bytes, void** out) {
   if (!out) {
     gfb::set_error("gf_malloc: null out");
@@ -78,12 +82,12 @@ extern "C" int gf_malloc(size_t bytes, void** out) {
   }
   *out = nullptr;
   if (bytes == 0) return GF_OK;
-  GF_CHECK_CUDA(cudaMalloc(out, bytes));
+  GF_CHECK_CUDA(gfb::scratch_alloc_raw(out, bytes, cudaStreamLegacy));
   return GF_OK;
 }
 
 extern "C" int gf_free(void* p) {
-  if (p) GF_CHECK_CUDA(cudaFree(p));
+  if (p) GF_CHECK_CUDA(cudaFreeAsync(p, cudaStreamLegacy));
   return GF_OK;
 }
 
