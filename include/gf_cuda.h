@@ -87,6 +87,9 @@ typedef struct gf_graph_info {
   int32_t n_small_rows;    /* CSR rows of degree 1..8: packed several per warp, one lane group
                               each (just before the empty rows in the order) */
   int32_t n_small_cols;
+  int32_t cta_blocks_rows; /* CTA-bucket blocks of the row pass: > n_cta_rows when super rows
+                              are split over several CTAs (multi-CTA split) */
+  int32_t cta_blocks_cols;
 } gf_graph_info;
 
 const char* gf_last_error(void);
@@ -139,6 +142,13 @@ int gf_graph_create_split(int64_t num_nodes, int64_t e_csr, const int32_t* d_row
 int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src, const int64_t* d_dst,
                        int64_t* d_row_ptr, int64_t* d_col, int64_t* d_csc_ptr,
                        int64_t* d_csc_row, int64_t* d_csc_perm, int64_t* bad, void* stream);
+/* Multi-CTA split of super rows / columns: a CTA-bucket row of degree d runs
+ * on ceil(d / split_len) CTAs (slice states merged in slice order by the
+ * last one).  Default split_len = max(cta_threshold, ceil(E / (148 * 4))) of
+ * the graph's own edge count; a row-sharded graph takes the unsharded
+ * graph's value here so its per-row reduction order, hence its results, stay
+ * bitwise equal to 1 GPU.  Not concurrent with launches on the graph. */
+int gf_graph_set_split_len(gf_graph_t g, int64_t split_len, void* stream);
 int gf_graph_destroy(gf_graph_t g);
 int gf_graph_get_info(gf_graph_t g, gf_graph_info* info);
 /* Copy the device schedules to host (row_order[n], col_order[n]; int32). */

@@ -34,7 +34,8 @@ class GraphInfo(C.Structure):
                 ("cta_threshold", C.c_int32), ("n_cta_rows", C.c_int32),
                 ("n_empty_rows", C.c_int32), ("n_cta_cols", C.c_int32),
                 ("n_empty_cols", C.c_int32), ("device", C.c_int32),
-                ("n_small_rows", C.c_int32), ("n_small_cols", C.c_int32)]
+                ("n_small_rows", C.c_int32), ("n_small_cols", C.c_int32),
+                ("cta_blocks_rows", C.c_int32), ("cta_blocks_cols", C.c_int32)]
 
 
 # Every symbol include/gf_cuda.h declares, with its ctypes signature.
@@ -87,6 +88,7 @@ SIGNATURES = {
                                           C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gf_measure_metrics": (C.c_int, [C.c_void_p, C.c_void_p, _vp, C.POINTER(C.c_char_p),
                                      C.c_int32, C.POINTER(C.c_double)]),
+    "gf_graph_set_split_len": (C.c_int, [_vp, C.c_int64, _vp]),
     "gf_l2_persist": (C.c_int, [C.c_size_t]),
     "gf_l2_persist_get": (C.c_int, [C.POINTER(C.c_size_t)]),
     "gf_l2_reset_persisting": (C.c_int, []),

@@ -101,7 +101,7 @@ __device__ __forceinline__ void warp_sum(T (&x)[NV]) {
 template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
 __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
-                                        const int nrows) {
+                                        const int nrows, const int4 ct) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -123,7 +123,10 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const int4 rsnn = r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
   const int v = rs.x;
   int eb = rs.y, ee = rs.z;
-  if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  if (cta) {
+    if (ct.z > 1) split_range(eb, ee, ct.z, ct.y, eb, ee);  // this CTA's slice of a split row
+    split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  }
   if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
 
   const int h = c / a.LPH;
@@ -320,6 +323,17 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
 
   if (!pk) warp_sum<T, LPE, NA>(acc);
   if (cta && !cta_sum<T, LPE, NA>(acc, warp, c, sub)) return;
+  if (cta && ct.z > 1) {  // split row: the last CTA sums the slices in slice order
+    if (!split_publish<NA>(a.part, a.part_cnt, ct, c, LPE, acc, sub == 0)) return;
+    T x[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = T(0);
+    for (int k = 0; k < ct.z; ++k) {
+      split_load<NA>(a.part, ct, k, c, LPE, x);
+#pragma unroll
+      for (int j = 0; j < NA; ++j) acc[j] += x[j];
+    }
+  }
   const bool writer = pk ? live : sub == 0;
 
   if constexpr (VAR == GF_DOT) {
@@ -343,19 +357,22 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
 #define GF_BWD_DISPATCH(ROWFN)                                                                  \
   constexpr int EPW = 32 / LPE;                                                                 \
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;                                   \
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);                                 \
-  if (cta) {                                                                                    \
-    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, true, blockIdx.x, true, 1);               \
-  } else if (blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {                         \
-    const int slot = a.n_cta + ((blockIdx.x - a.n_cta) * kWarpsPerBlock + warp) * a.rpw;        \
+  const int cb = a.cta_tab ? a.cta_blocks : a.n_cta;                                            \
+  const int4 one = make_int4(0, 0, 1, -1);                                                      \
+  if (blockIdx.x < static_cast<unsigned>(cb)) {                                                 \
+    const int4 ct = a.cta_tab ? __ldg(a.cta_tab + blockIdx.x) : make_int4(blockIdx.x, 0, 1, -1); \
+    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, true, ct.x, true, 1, ct);                 \
+  } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {                              \
+    const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;             \
     if (slot >= a.pk0) return;                                                                  \
-    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, false, slot, true, min(a.rpw, a.pk0 - slot)); \
+    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, false, slot, true, min(a.rpw, a.pk0 - slot), \
+                                       one);                                                    \
   } else if constexpr (EPW > 1) {                                                               \
-    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW + \
+    const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +    \
                      lane / LPE;                                                                \
     const bool live = slot < a.n;                                                               \
     if (!__any_sync(kFull, live)) return;                                                       \
-    ROWFN<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1);                     \
+    ROWFN<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1, one);                \
   }
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
@@ -367,7 +384,8 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_r
 template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
 __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
-                                        int /*nrows: pass B runs one column per warp, see below*/) {
+                                        int /*nrows: pass B runs one column per warp, see below*/,
+                                        const int4 ct) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -379,7 +397,10 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   // budget (4 CTAs/SM) either spills; the launcher keeps rpw = 1.
   const int u = live ? __ldg(a.order + slot) : 0;
   int sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
-  if (cta) split_range(sb, se, kWarpsPerBlock, warp, sb, se);
+  if (cta) {
+    if (ct.z > 1) split_range(sb, se, ct.z, ct.y, sb, se);  // this CTA's slice of a split column
+    split_range(sb, se, kWarpsPerBlock, warp, sb, se);
+  }
 
   const int h = c / a.LPH;
   const int off = h * a.D + (c % a.LPH) * NE;
@@ -562,6 +583,17 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
 
   if (!pk) warp_sum<T, LPE, NT>(all);
   if (cta && !cta_sum<T, LPE, NT>(all, warp, c, sub)) return;
+  if (cta && ct.z > 1) {  // split column: the last CTA sums the slices in slice order
+    if (!split_publish<NT>(a.part, a.part_cnt, ct, c, LPE, all, sub == 0)) return;
+    T x[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) all[j] = T(0);
+    for (int k = 0; k < ct.z; ++k) {
+      split_load<NT>(a.part, ct, k, c, LPE, x);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) all[j] += x[j];
+    }
+  }
 
   T g[NE];
   if constexpr (VAR == GF_DOT) {
@@ -588,17 +620,20 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
   // push pass B past its 64-register budget
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  if (cta || blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
-    const int slot = cta ? blockIdx.x : a.n_cta + (blockIdx.x - a.n_cta) * kWarpsPerBlock + warp;
+  const int cb = a.cta_tab ? a.cta_blocks : a.n_cta;
+  const bool cta = blockIdx.x < static_cast<unsigned>(cb);
+  if (cta || blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {
+    const int4 ct = !cta ? make_int4(0, 0, 1, -1)
+                         : (a.cta_tab ? __ldg(a.cta_tab + blockIdx.x) : make_int4(blockIdx.x, 0, 1, -1));
+    const int slot = cta ? ct.x : a.n_cta + (blockIdx.x - cb) * kWarpsPerBlock + warp;
     if (!cta && slot >= a.pk0) return;
-    bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1);
+    bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1, ct);
   } else if constexpr (EPW > 1) {
-    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW +
+    const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +
                      lane / LPE;
     const bool live = slot < a.n;
     if (!__any_sync(kFull, live)) return;
-    bwd_col<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1);
+    bwd_col<T, CB, LPE, CPL, VAR, true>(a, lane, warp, false, slot, live, 1, make_int4(0, 0, 1, -1));
   }
 }
 
@@ -811,6 +846,8 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   BwdArgs<T> ra = a, ca = a;
   ra.ptr = g.row_ptr, ra.idx = g.col, ra.order = g.row_order, ra.n_cta = g.n_cta_rows;
   ca.ptr = g.csc_ptr, ca.idx = g.csc_row, ca.order = g.col_order, ca.n_cta = g.n_cta_cols;
+  ra.cta_tab = g.row_cta, ra.cta_blocks = g.row_cta_blocks, ra.parts = g.row_parts;
+  ca.cta_tab = g.col_cta, ca.cta_blocks = g.col_cta_blocks, ca.parts = g.col_parts;
   ra.sched = g.row_sched, ca.sched = g.col_sched;
   ra.n = g.active_rows();
   ca.n = g.active_cols();
@@ -837,10 +874,37 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
     if (&x == &ra) x.rpw = rows_per_warp(g.e, g.n, x.pk0 - x.n_cta);
     x.wblocks = (x.pk0 - x.n_cta + kWarpsPerBlock * x.rpw - 1) / (kWarpsPerBlock * x.rpw);
     const int per_block = kWarpsPerBlock * epw;
-    return x.n_cta + x.wblocks + (x.n - x.pk0 + per_block - 1) / per_block;
+    const int cta_blocks = x.cta_tab ? x.cta_blocks : x.n_cta;
+    return cta_blocks + x.wblocks + (x.n - x.pk0 + per_block - 1) / per_block;
   };
   const int rb = (do_a && fast_a) ? buckets(ra, g.n_small_rows, g.n_empty_rows) : 0;
   const int cbk = (do_b && fast_b) ? buckets(ca, g.n_small_cols, g.n_empty_cols) : 0;
+  // split super rows / columns: slice partials + arrival counters
+  const size_t ne = fs.ok ? static_cast<size_t>(fs.cpl) * (fs.cb / sizeof(T)) : 0;
+  auto parts = [&](BwdArgs<T>& x, size_t nv) -> int {
+    if (!x.cta_tab || x.parts == 0) return GF_OK;
+    GF_CHECK_CUDA(scratch_alloc(&x.part, sizeof(T) * x.parts * fs.lpe * nv, s));
+    GF_CHECK_CUDA(scratch_alloc(&x.part_cnt, sizeof(unsigned) * x.parts, s));
+    GF_CHECK_CUDA(cudaMemsetAsync(x.part_cnt, 0, sizeof(unsigned) * x.parts, s));
+    return GF_OK;
+  };
+  struct PartFree {
+    BwdArgs<T>& r;
+    BwdArgs<T>& c;
+    cudaStream_t s;
+    ~PartFree() {
+      for (BwdArgs<T>* x : {&r, &c}) {
+        if (x->part) cudaFreeAsync(x->part, s);
+        if (x->part_cnt) cudaFreeAsync(x->part_cnt, s);
+      }
+    }
+  } part_free{ra, ca, s};
+  if (rb) {
+    if (int rc = parts(ra, dot ? ne : 1)) return rc;
+  }
+  if (cbk) {
+    if (int rc = parts(ca, ne + (dot ? ne : 1))) return rc;
+  }
   if (rb || cbk) {
     int rc = GF_OK;
     switch (fs.cb * 1000 + fs.lpe * 10 + fs.cpl) {

@@ -64,7 +64,7 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
 template <typename T, int CB, int LPE, int CPL, int VAR, int MODE, bool PK>
 __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
-                                        const int nrows) {
+                                        const int nrows, const int4 ct) {
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
@@ -92,7 +92,10 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const int4 rsnn = GF_ROWPIPE && r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
   const int v = rs.x;
   int eb = rs.y, ee = rs.z;
-  if (cta) split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  if (cta) {
+    if (ct.z > 1) split_range(eb, ee, ct.z, ct.y, eb, ee);  // this CTA's slice of a split row
+    split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
+  }
   if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
 
   // Destination-side operands stay in registers for the whole row.
@@ -358,6 +361,30 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
         }
       }
     }
+    if (ct.z > 1) {  // split row: publish this slice; the last CTA merges all slices
+      T st[2 + NE];
+      st[0] = m;
+      st[1] = l;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) st[2 + i] = acc[i];
+      if (!split_publish<2 + NE>(a.part, a.part_cnt, ct, c, LPE, st, sub == 0)) return;
+      m = ninf<T>();
+      l = T(0);
+#pragma unroll
+      for (int i = 0; i < NE; ++i) acc[i] = T(0);
+      for (int k = 0; k < ct.z; ++k) {
+        split_load<2 + NE>(a.part, ct, k, c, LPE, st);
+        T acc2[NE];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) acc2[i] = st[2 + i];
+        if constexpr (MODE >= 2) {
+#pragma unroll
+          for (int i = 0; i < NE; ++i) acc[i] += acc2[i];
+        } else {
+          merge_state<T, NE>(m, l, acc, st[0], st[1], acc2);
+        }
+      }
+    }
   }
 
   if (pk ? live : sub == 0) {
@@ -388,20 +415,22 @@ template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool cta = blockIdx.x < static_cast<unsigned>(a.n_cta);
-  if (cta) {
-    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, true, blockIdx.x, true, 1);
-  } else if (blockIdx.x < static_cast<unsigned>(a.n_cta + a.wblocks)) {
-    const int slot = a.n_cta + ((blockIdx.x - a.n_cta) * kWarpsPerBlock + warp) * a.rpw;
+  const int cb = a.cta_tab ? a.cta_blocks : a.n_cta;  // CTA-bucket blocks
+  const int4 one = make_int4(0, 0, 1, -1);
+  if (blockIdx.x < static_cast<unsigned>(cb)) {
+    const int4 ct = a.cta_tab ? __ldg(a.cta_tab + blockIdx.x) : make_int4(blockIdx.x, 0, 1, -1);
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, true, ct.x, true, 1, ct);
+  } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {
+    const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;
     if (slot >= a.pk0) return;
     fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, false, slot, true,
-                                               min(a.rpw, a.pk0 - slot));
+                                               min(a.rpw, a.pk0 - slot), one);
   } else if constexpr (EPW > 1) {
-    const int slot = a.pk0 + ((blockIdx.x - a.n_cta - a.wblocks) * kWarpsPerBlock + warp) * EPW +
+    const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +
                      lane / LPE;
     const bool live = slot < a.n;
     if (!__any_sync(kFull, live)) return;
-    fwd_row<T, CB, LPE, CPL, VAR, MODE, true>(a, lane, warp, false, slot, live, 1);
+    fwd_row<T, CB, LPE, CPL, VAR, MODE, true>(a, lane, warp, false, slot, live, 1, one);
   }
 }
 
@@ -587,7 +616,23 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     a.rpw = GF_ROWPIPE ? rows_per_warp(a.e, g.n, a.pk0 - a.n_cta) : 1;
     a.wblocks = (a.pk0 - a.n_cta + kWarpsPerBlock * a.rpw - 1) / (kWarpsPerBlock * a.rpw);
     const int rows_per_block = kWarpsPerBlock * epw;
-    const int blocks = a.n_cta + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;
+    const int cta_blocks = a.cta_tab ? a.cta_blocks : a.n_cta;
+    const int blocks = cta_blocks + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;
+    // split super rows: slice states + arrival counters (stream-ordered scratch)
+    if (a.cta_tab && a.parts > 0) {
+      const size_t nv = 2 + static_cast<size_t>(fs.cpl) * (fs.cb / sizeof(T));
+      GF_CHECK_CUDA(scratch_alloc(&a.part, sizeof(T) * a.parts * fs.lpe * nv, s));
+      GF_CHECK_CUDA(scratch_alloc(&a.part_cnt, sizeof(unsigned) * a.parts, s));
+      GF_CHECK_CUDA(cudaMemsetAsync(a.part_cnt, 0, sizeof(unsigned) * a.parts, s));
+    }
+    struct PartFree {
+      FwdArgs<T>& a;
+      cudaStream_t s;
+      ~PartFree() {
+        if (a.part) cudaFreeAsync(a.part, s);
+        if (a.part_cnt) cudaFreeAsync(a.part_cnt, s);
+      }
+    } part_free{a, s};
     const int key = fs.cb * 1000 + fs.lpe * 10 + fs.cpl;
     switch (key) {
       case 32011: return launch_fast_fwd<T, 32, 1, 1>(a, variant, mode, blocks, s);

@@ -140,6 +140,9 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
   a.e = g.e;
   a.n = g.active_rows();
   a.n_cta = g.n_cta_rows;
+  a.cta_tab = g.row_cta;
+  a.cta_blocks = g.row_cta_blocks;
+  a.parts = g.row_parts;
   a.H = d.heads;
   a.D = d.head_dim;
   a.F = d.heads * d.head_dim;

@@ -333,6 +333,42 @@ __device__ __forceinline__ void generic_row_setup(const A& a, int v, int lane, c
   }
 }
 
+// ------------------------------------------------- multi-CTA split rows --
+// A super row / column split over ct.z CTAs (ct = {slot, slice, slices, first
+// partial}, DevGraph::row_cta): each CTA publishes its slice's state (NV
+// values per lane group c of LPE) to part[], then the LAST CTA to arrive
+// (per-row arrival counter) merges all slices in slice order 0..z-1, so the
+// result does not depend on which CTA arrives last (deterministic).  Called by
+// every lane of the CTA's merging warp; `writer` lanes own a lane group.
+// Returns true in the last CTA (whose lanes then call split_load).
+template <int NV, typename T>
+__device__ __forceinline__ bool split_publish(T* __restrict__ part, unsigned* __restrict__ cnt,
+                                              const int4 ct, int c, int lpe, const T (&x)[NV],
+                                              bool writer) {
+  if (writer) {
+    T* p = part + (static_cast<size_t>(ct.w + ct.y) * lpe + c) * NV;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) p[i] = x[i];
+  }
+  __threadfence();
+  __syncwarp();
+  unsigned prev = 0;
+  if ((threadIdx.x & 31) == 0) prev = atomicAdd(cnt + ct.w, 1u);
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev + 1 != static_cast<unsigned>(ct.z)) return false;
+  __threadfence();
+  if ((threadIdx.x & 31) == 0) cnt[ct.w] = 0;  // re-armed for the next launch
+  return true;
+}
+
+template <int NV, typename T>
+__device__ __forceinline__ void split_load(const T* __restrict__ part, const int4 ct, int slice,
+                                           int c, int lpe, T (&x)[NV]) {
+  const T* p = part + (static_cast<size_t>(ct.w + slice) * lpe + c) * NV;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) x[i] = __ldcg(p + i);  // L2: written by other SMs
+}
+
 // Balanced split of [b, e) into `parts` contiguous slices (first `rem` get +1),
 // the same rule the reference uses for warp_balance (schedule.cpp:42-60).
 __device__ __forceinline__ void split_range(int b, int e, int parts, int i, int& sb, int& se) {

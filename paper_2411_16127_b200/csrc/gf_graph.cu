@@ -124,6 +124,34 @@ int build_sched(const int32_t* order, const int32_t* ptr, int n, int4** out, cud
   return GF_OK;
 }
 
+// CTA-bucket block table of one pass: the first n_cta schedule slots are the
+// CTA rows (degree-descending); a row of degree d gets ceil(d / split_len)
+// blocks {slot, slice, slices, first partial}; single-slice rows carry -1.
+int build_cta_table(const int4* sched, int n_cta, int64_t len, int4** tab, int32_t& blocks,
+                    int32_t& parts, cudaStream_t s) {
+  blocks = parts = 0;
+  cudaFree(*tab);
+  *tab = nullptr;
+  if (n_cta == 0) return GF_OK;
+  std::vector<int4> h(static_cast<size_t>(n_cta));
+  GF_CHECK_CUDA(cudaMemcpyAsync(h.data(), sched, sizeof(int4) * n_cta, cudaMemcpyDeviceToHost, s));
+  GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  std::vector<int4> t;
+  t.reserve(static_cast<size_t>(n_cta));
+  for (int r = 0; r < n_cta; ++r) {
+    const int64_t d = static_cast<int64_t>(h[r].z) - h[r].y;
+    const int ns = static_cast<int>(std::max<int64_t>(1, (d + len - 1) / len));
+    const int base = ns > 1 ? parts : -1;
+    for (int k = 0; k < ns; ++k) t.push_back(make_int4(r, k, ns, base));
+    if (ns > 1) parts += ns;
+  }
+  blocks = static_cast<int32_t>(t.size());
+  GF_CHECK_CUDA(cudaMalloc(tab, sizeof(int4) * t.size()));
+  GF_CHECK_CUDA(cudaMemcpyAsync(*tab, t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice, s));
+  GF_CHECK_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
 int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
   g->cta_threshold = thr > 0 ? thr : auto_cta_threshold(std::max<int64_t>(g->e, g->e_csc));
   GF_CHECK_CUDA(cudaGetDevice(&g->device));
@@ -137,6 +165,12 @@ int finish_graph(DevGraph* g, int thr, cudaStream_t s) {
   if (rc) return rc;
   if ((rc = build_sched(g->row_order, g->row_ptr, g->n, &g->row_sched, s))) return rc;
   if ((rc = build_sched(g->col_order, g->csc_ptr, g->n, &g->col_sched, s))) return rc;
+  if ((rc = build_cta_table(g->row_sched, g->n_cta_rows, split_len(g->e, g->cta_threshold),
+                            &g->row_cta, g->row_cta_blocks, g->row_parts, s)))
+    return rc;
+  if ((rc = build_cta_table(g->col_sched, g->n_cta_cols, split_len(g->e_csc, g->cta_threshold),
+                            &g->col_cta, g->col_cta_blocks, g->col_parts, s)))
+    return rc;
   GF_CHECK_CUDA(cudaStreamSynchronize(s));
   return GF_OK;
 }
@@ -151,6 +185,8 @@ void free_graph(DevGraph* g) {
   cudaFree(g->col_order);
   cudaFree(g->row_sched);
   cudaFree(g->col_sched);
+  cudaFree(g->row_cta);
+  cudaFree(g->col_cta);
   cudaFree(g->coo_dst);
   cudaFree(g->csc_perm);
   delete g;
@@ -330,6 +366,8 @@ extern "C" int gf_graph_get_info(gf_graph_t g, gf_graph_info* info) {
   info->device = g->device;
   info->n_small_rows = g->n_small_rows;
   info->n_small_cols = g->n_small_cols;
+  info->cta_blocks_rows = g->row_cta_blocks;
+  info->cta_blocks_cols = g->col_cta_blocks;
   return GF_OK;
 }
 
@@ -429,3 +467,17 @@ extern "C" int gf_from_coo_device(int64_t n, int64_t e, const int64_t* d_src,
   return rc;
 }
 
+
+extern "C" int gf_graph_set_split_len(gf_graph_t g, int64_t split_len, void* stream) {
+  if (!g || split_len < 1) {
+    gfb::set_error("gf_graph_set_split_len: null graph or split_len < 1");
+    return GF_ERR_INVALID;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  int rc = gfb::build_cta_table(g->row_sched, g->n_cta_rows, split_len, &g->row_cta,
+                                g->row_cta_blocks, g->row_parts, s);
+  if (!rc)
+    rc = gfb::build_cta_table(g->col_sched, g->n_cta_cols, split_len, &g->col_cta,
+                              g->col_cta_blocks, g->col_parts, s);
+  return rc;
+}

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "gf_cuda.h"
@@ -76,6 +77,15 @@ struct DevGraph {
                                 // the edge-parallel strategies; graph-owned)
   int32_t* csc_perm = nullptr;  // CSC slot -> CSR edge id (reference csc_edge_perm), built
                                 // on first use by the unfused backward ops; graph-owned
+  // Multi-CTA split of super rows / columns: the CTA bucket's blocks, one
+  // int4 {slot, slice, slices, first partial} per block.  A row of degree d
+  // takes ceil(d / split_len) CTAs (split_len = max(cta_threshold,
+  // E / (148 * 4))); split rows publish per-slice partial states that the
+  // last-arriving CTA merges in slice order (gf_attn_fwd.cuh split_publish).
+  int4* row_cta = nullptr;
+  int4* col_cta = nullptr;
+  int32_t row_cta_blocks = 0, col_cta_blocks = 0;  // CTA-bucket blocks
+  int32_t row_parts = 0, col_parts = 0;            // partial slots of split rows / columns
   int32_t e_csc = 0;        // CSC edge count (== e unless row-sharded)
   bool skip_empty = false;  // do not visit rows / columns without edges
   /// Rows (resp. columns) a pass visits: the empty ones trail the order.
@@ -148,6 +158,14 @@ inline int rows_per_warp(int64_t edges, int64_t nodes, int64_t warp_rows) {
   return r >= 8 ? 8 : r >= 4 ? 4 : r >= 2 ? 2 : 1;
 }
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
+// Edges per CTA slice of a split row: no CTA of a pass holds more than ~1/4
+// of one SM's share of the edges (148 SMs), and never fewer than a CTA row.
+// GF_SPLIT_LEN=<edges> overrides (A/B; a huge value disables splitting).
+inline int64_t split_len(int64_t e, int cta_threshold) {
+  const char* env = std::getenv("GF_SPLIT_LEN");
+  if (env && *env) return std::max<int64_t>(1, std::atoll(env));
+  return std::max<int64_t>(std::max(cta_threshold, 1), (e + 148 * 4 - 1) / (148 * 4));
+}
 
 // ---------------------------------------------------------- kernel params --
 // Lane geometry of the fast path (see fast_shape): a lane owns CPL chunks of
@@ -173,6 +191,12 @@ struct FwdArgs {
   int64_t e = 0;                 // edges of that view (rows_per_warp)
   const T* ES = nullptr;  // E x H edge scores (PMF) / probabilities (unfused), CSR order
   const int32_t* eperm = nullptr;  // MODE 3: slot -> CSR edge id of ES (CSC passes)
+  // multi-CTA split rows (DevGraph::row_cta); cta_tab == nullptr: one CTA per
+  // CTA-bucket row (block b -> slot b)
+  const int4* cta_tab = nullptr;
+  int cta_blocks = 0, parts = 0;
+  T* part = nullptr;           // parts x LPE x (2 + NE) slice states
+  unsigned* part_cnt = nullptr;  // arrivals per split row (indexed by its first partial)
 };
 
 template <typename T>
@@ -196,6 +220,10 @@ struct BwdArgs {
   T* dV;     // pass B
   int pk0 = 0, wblocks = 0;  // packed bucket: first slot; #blocks of the warp bucket
   int rpw = 1;               // warp-bucket rows per warp
+  const int4* cta_tab = nullptr;  // multi-CTA split (as FwdArgs)
+  int cta_blocks = 0, parts = 0;
+  T* part = nullptr;
+  unsigned* part_cnt = nullptr;
 };
 
 // Launchers (defined in gf_attn_fwd.cuh / gf_attn_bwd.cuh).

@@ -182,6 +182,9 @@ FwdArgs<T> base_args(const DevGraph& g, int H, int D, bool csc) {
   a.e = csc ? g.e_csc : g.e;
   a.n = csc ? g.active_cols() : g.active_rows();
   a.n_cta = csc ? g.n_cta_cols : g.n_cta_rows;
+  a.cta_tab = csc ? g.col_cta : g.row_cta;
+  a.cta_blocks = csc ? g.col_cta_blocks : g.row_cta_blocks;
+  a.parts = csc ? g.col_parts : g.row_parts;
   a.H = H;
   a.D = D;
   a.F = H * D;

@@ -93,6 +93,15 @@ class DeviceGraph:
                                           _stream(stream), C.byref(h)), "gf_graph_create_split")
         return cls(h)
 
+    def set_split_len(self, split_len, stream=None):
+        """Edges per CTA slice of a split super row / column
+        (gf_graph_set_split_len); rebuilds the CTA tables."""
+        check(lib().gf_graph_set_split_len(self._h, int(split_len), _stream(stream)),
+              "gf_graph_set_split_len")
+        info = GraphInfo()
+        check(lib().gf_graph_get_info(self._h, C.byref(info)), "gf_graph_get_info")
+        self.info = info
+
     def schedule(self):
         """(row_order, col_order) as int32 numpy arrays (degree-descending)."""
         ro = np.zeros(max(self.n, 1), np.int32)
@@ -115,6 +124,13 @@ class DeviceGraph:
             self.close()
         except Exception:
             pass
+
+
+def default_split_len(e, cta_threshold=0):
+    """The library's default split_len for a graph of e edges (gf_cuda.h):
+    max(cta_threshold or the automatic one, ceil(e / (148 * 4)))."""
+    thr = cta_threshold if cta_threshold > 0 else min(16384, max(1024, e // 28416))
+    return max(thr, -(-e // (148 * 4)))
 
 
 def from_coo_device(n: int, src: torch.Tensor, dst: torch.Tensor, stream=None):
@@ -433,3 +449,4 @@ def measure_metrics(fn, metrics, prep=None):
     check(lib().gf_measure_metrics(C.cast(pcb, C.c_void_p) if pcb else None, C.cast(cb, C.c_void_p),
                                    None, names, len(metrics), vals), "gf_measure_metrics")
     return {m: float(v) for m, v in zip(metrics, vals)}
+

@@ -48,6 +48,7 @@ class RowShard:
     col: torch.Tensor      # int32 [e_csr]
     csc_ptr: torch.Tensor  # int32 [world*R + 1]: CSC of the owned columns
     csc_row: torch.Tensor  # int32 [e_csc]
+    e_total: int = 0       # edges of the unsharded graph (sets the multi-CTA split_len)
 
     @property
     def n_padded(self) -> int:
@@ -95,7 +96,7 @@ class RowShard:
 
         rp, c = side(row_ptr, col)
         cp, cr = side(csc_ptr, csc_row)
-        return cls(rank, world, n, bounds, R, rp, c, cp, cr)
+        return cls(rank, world, n, bounds, R, rp, c, cp, cr, int(row_ptr[-1]))
 
     def to_padded(self, x: torch.Tensor) -> torch.Tensor:
         """Full node table (original ids) -> padded table (world*R rows)."""
@@ -111,12 +112,18 @@ class RowShard:
         return torch.cat(parts, 0)
 
     def device_graph(self, cta_threshold: int = 0, stream=None):
-        """gf_graph_t over the padded id space; empty (foreign) rows skipped."""
-        from .fused import DeviceGraph
+        """gf_graph_t over the padded id space; empty (foreign) rows skipped.
+        Super rows are split over CTAs exactly as in the unsharded graph
+        (split_len from the total edge count), so owned rows / columns keep
+        the 1-GPU reduction order."""
+        from .fused import DeviceGraph, default_split_len
 
-        return DeviceGraph.from_split(self.n_padded, self.row_ptr, self.col, self.csc_ptr,
-                                      self.csc_row, cta_threshold=cta_threshold, skip_empty=True,
-                                      stream=stream)
+        dg = DeviceGraph.from_split(self.n_padded, self.row_ptr, self.col, self.csc_ptr,
+                                    self.csc_row, cta_threshold=cta_threshold, skip_empty=True,
+                                    stream=stream)
+        if self.e_total:
+            dg.set_split_len(default_split_len(self.e_total, cta_threshold), stream=stream)
+        return dg
 
 
 def all_gather_rows(table: torch.Tensor, shard: RowShard, group=None, async_op=False):

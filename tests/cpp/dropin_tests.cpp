@@ -436,8 +436,8 @@ static void bench_cases() {
   EXPECT(std::count(csv.begin(), csv.end(), '\n') == static_cast<long>(1 + report.rows.size()));
   EXPECT(report_markdown(report).find("| mode |") != std::string::npos);
   const std::string dcsv = report_csv_device(report);
-  EXPECT(dcsv.find(",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization\n") !=
-         std::string::npos);
+  EXPECT(dcsv.find(",device_ms,device_speedup_vs_unfused,device_bandwidth_utilization,"
+                   "device_dram_bytes\n") != std::string::npos);
 
   BenchConfig g = cfg;  // auto never picks PMF for additive attention
   g.model = "gat";
