@@ -229,7 +229,7 @@ def gen_graph_host(name, seed=0, rows=None):
 
 
 # ----------------------------------------------------------- measurement --
-def algorithmic_bytes(kernel, layer, n, e, H, D, b=4, idx=4):
+def algorithmic_bytes(kernel, layer, n, e, H, D, b=4, idx=4, from_v=False):
     """Per-launch algorithmic bytes (SURVEY §8(d) gather
     model with this design's stats layout): every gathered row counted per
     edge, every owned row once, index arrays once."""
@@ -238,6 +238,13 @@ def algorithmic_bytes(kernel, layer, n, e, H, D, b=4, idx=4):
     qk = F if dot else H  # Q|el and K|er width
     rec = 4 * H  # softmax record {m, log2 l, aux, delta} per head
     topo = idx * (2 * n + 1 + e)  # row pointer, schedule, neighbour ids
+    if from_v:  # GAT layer form: el / er from V rows (own V row replaces er)
+        if kernel == "fwd":
+            return topo + b * (e * F + n * (F + F + rec))
+        if kernel == "bwd_rows":
+            return topo + b * (e * F + n * (2 * F + rec + H + H))
+        if kernel == "bwd_cols":
+            return topo + b * (e * (F + rec) + n * (2 * F + qk))
     if kernel == "fwd":  # gather V, Q|el of src; own K|er; write O + records
         return topo + b * (e * (F + qk) + n * (qk + F + rec))
     if kernel == "bwd_rows":  # gather V, Q|el of src; own dO, O, K (dot), record; write dK|der, delta
@@ -342,22 +349,24 @@ def l2_request_costs():
     return t32 - b, b, g32, g128
 
 
-def gathered_rows(kernel, layer, H, D, b=4):
+def gathered_rows(kernel, layer, H, D, b=4, from_v=False):
     """Row sizes (bytes) each edge gathers in one launch."""
     F = H * D
     rec = 16 * H if b == 4 else 32 * H
+    if layer == "gat" and from_v:  # no el gather: logits from the V row
+        return {"fwd": [b * F], "bwd_rows": [b * F], "bwd_cols": [b * F, rec]}[kernel]
     if layer == "gat":
         return {"fwd": [b * F, b * H], "bwd_rows": [b * F, b * H], "bwd_cols": [b * F, rec]}[kernel]
     return {"fwd": [b * F, b * F], "bwd_rows": [b * F, b * F],
             "bwd_cols": [b * F, b * F, rec]}[kernel]
 
 
-def l2_request_model_ms(kernel, layer, H, D, e, a_ps, b_ps):
+def l2_request_model_ms(kernel, layer, H, D, e, a_ps, b_ps, from_v=False):
     """Modelled launch time when every gather is an L2 hit: per edge and
     gathered row, a line-request cost per 128 B line touched plus a sector
     cost per 32 B sector."""
     t = 0.0
-    for rb in gathered_rows(kernel, layer, H, D):
+    for rb in gathered_rows(kernel, layer, H, D, from_v=from_v):
         t += a_ps * max(1, -(-rb // 128)) + b_ps * max(1, -(-rb // 32))
     return e * t * 1e-9
 
@@ -565,6 +574,9 @@ def main(argv=None):
                     help="opt-in persisting-L2 set-aside for the evict-last node tables "
                          "(gf_l2_persist); 0 = none.  The line also reports the value without it")
     ap.add_argument("--cta-threshold", type=int, default=0)
+    ap.add_argument("--gat-tables", action="store_true",
+                    help="GAT in the reference operator's table form (el / er per node gathered) "
+                         "instead of the layer form (logits from the gathered V rows)")
     ap.add_argument("--no-api", action="store_true",
                     help="skip timing the reference-facing C++ API path (run_strategy + "
                          "fused_backward per head, host buffers)")
@@ -805,8 +817,11 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
                 pt.barrier()
                 # el / er of every row from the complete table (deterministic per
                 # row, so identical to the owners' values): no logit exchange
-                fused.gat_logits(Hf, al, ar, H, D, stream=stream, el=EL, er=ER)
-                q, k, v = EL, ER, Hf
+                if spec.logits_from_v:  # logits computed in the attention kernels
+                    q, k, v = al, ar, Hf
+                else:
+                    fused.gat_logits(Hf, al, ar, H, D, stream=stream, el=EL, er=ER)
+                    q, k, v = EL, ER, Hf
             else:
                 for w_, name in ((Wq, "Q"), (Wk, "K"), (Wv, "V")):
                     fused.gemm_bcast(Xr, w_, pt.dests(name), stream=stream)
@@ -815,8 +830,11 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             later = [all_gather_rows(dO, shard, async_op=True)]
         elif gat:
             fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
-            fused.gat_logits(Hf[rows], al, ar, H, D, stream=stream, el=EL[rows], er=ER[rows])
-            q, k, v = EL, ER, Hf
+            if spec.logits_from_v:  # logits computed in the attention kernels
+                q, k, v = al, ar, Hf
+            else:
+                fused.gat_logits(Hf[rows], al, ar, H, D, stream=stream, el=EL[rows], er=ER[rows])
+                q, k, v = EL, ER, Hf
         else:
             fused.gemm(Xr, Wq, out=Qb[rows], stream=stream)
             fused.gemm(Xr, Wk, out=Kb[rows], stream=stream)
@@ -1096,9 +1114,16 @@ def run_ours(args, cfg, rank, world, full=True):
     pre_coo_ms = (time.perf_counter() - t_pre) * 1e3
     del src, dst
     e = int(col.numel())
+    # GAT runs in its layer form by default: the attention logits are linear in
+    # the projected features (el = <H[u], a_l>, er = <H[v], a_r>, models.hpp:
+    # 116-125), so Q / K carry a_l / a_r and the kernels compute the logits
+    # from the V rows they gather (GF_FLAG_LOGITS_FROM_V).  --gat-tables runs
+    # the reference operator's table form (el / er given per node).
+    from_v = layer == "gat" and not args.gat_tables
+    node_qk = not from_v  # Q / K are node tables (else a_l / a_r vectors)
     spec = fused.AttnSpec("add" if layer == "gat" else "dot", H, D,
                           scale=(1.0 / np.sqrt(D)) if layer == "gt" else 1.0, slope=0.2,
-                          l2=layer == "agnn")
+                          l2=layer == "agnn", logits_from_v=from_v)
     F = H * D
     qk = spec.qk_width
     gen = torch.Generator(device=dev)
@@ -1108,7 +1133,10 @@ def run_ours(args, cfg, rank, world, full=True):
         return (torch.rand(*shape, device=dev, generator=gen) * 2 - 1) * amp
 
     amp = 2.0 if layer == "gat" else 1.0
-    Q, K, V, dO = u(n, qk, amp=amp), u(n, qk, amp=amp), u(n, F), u(n, F)
+    if from_v:
+        Q, K, V, dO = u(1, F), u(1, F), u(n, F), u(n, F)  # a_l, a_r, H, dO
+    else:
+        Q, K, V, dO = u(n, qk, amp=amp), u(n, qk, amp=amp), u(n, F), u(n, F)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream()
     shard = None
@@ -1119,7 +1147,8 @@ def run_ours(args, cfg, rank, world, full=True):
 
         shard = RowShard.build(n, row_ptr, col, csc_ptr, csc_row, rank, world)
         dg = shard.device_graph(cta_threshold=args.cta_threshold)
-        Q, K, V, dO = (shard.to_padded(x) for x in (Q, K, V, dO))
+        Q, K = (shard.to_padded(x) if node_qk else x for x in (Q, K))
+        V, dO = (shard.to_padded(x) for x in (V, dO))
         n_tab = shard.n_padded
     else:
         t_pre = time.perf_counter()
@@ -1167,7 +1196,7 @@ def run_ours(args, cfg, rank, world, full=True):
         if sharded and phased:
             R = shard.R
             blocks = {b: [torch.distributed.broadcast(t[b * R:(b + 1) * R], src=b, async_op=True)
-                          for t in (V, Q)] for b in range(world)}
+                          for t in (V,) + ((Q,) if node_qk else ())] for b in range(world)}
             later = [all_gather_rows(t, shard, async_op=True)
                      for t in (dO,) + ((K,) if layer != "gat" else ())]
             k += 1
@@ -1183,7 +1212,8 @@ def run_ours(args, cfg, rank, world, full=True):
             # exchange 1: source-side rows the forward gathers (V, Q|el) — waited
             # on; then dO and, for dot models, K (only pass B gathers them) are
             # issued on NCCL's stream and overlap the forward and pass A
-            first = [all_gather_rows(t, shard, async_op=True) for t in (V, Q)]
+            first = [all_gather_rows(t, shard, async_op=True)
+                     for t in (V,) + ((Q,) if node_qk else ())]
             later = [all_gather_rows(t, shard, async_op=True)
                      for t in (dO,) + ((K,) if layer != "gat" else ())]
             for w in first:
@@ -1243,6 +1273,26 @@ def run_ours(args, cfg, rank, world, full=True):
 
     ms_per_step = whole_job_ms(evs)
     value = e / (ms_per_step / 1e3) / 1e9
+    # GAT: the reference operator's table form (el / er given per node and
+    # gathered per edge) on the same graph and features, for comparison
+    table_form = None
+    if full and from_v and not sharded:
+        spec_t = fused.AttnSpec("add", H, D, slope=0.2)
+        EL, ER = fused.gat_logits(V, Q, K, H, D, stream=stream)
+        Qs, Ks = Q, K
+        Q, K, spec_l = EL, ER, spec
+        spec = spec_t
+        for _ in range(2):
+            step()
+        ms_t = whole_job_ms(timed(steps))
+        kt = {nm: round(statistics.mean(a[j].elapsed_time(a[j + 1]) for a in timed(5)), 4)
+              for j, nm in enumerate(("fwd", "bwd_rows", "bwd_cols"))}
+        Q, K, spec = Qs, Ks, spec_l
+        del EL, ER
+        table_form = {"value": e / (ms_t / 1e3) / 1e9, "ms_per_step": ms_t, "kernels_ms": kt,
+                      "note": "the same GAT step with el / er precomputed per node "
+                              "(gf_gat_logits) and gathered per edge: the reference operator's "
+                              "Add-SDDMM form (run_strategy with el, er inputs)"}
     # The same timed loop without the persisting-L2 set-aside (the library's
     # default: bench.py opts in with gf_l2_persist), so the carve-out's share
     # of the headline is on record.
@@ -1328,14 +1378,16 @@ def run_ours(args, cfg, rank, world, full=True):
         # pinned host memory, runs the step (NCCL all-gathers included) and
         # downloads its own rows of O, dQ|del, dK|der, dV; max over ranks.
         own = shard.rows
-        hin = [x[own].cpu().pin_memory() for x in (Q, K, V, dO)]
+        sel = lambda x, node=True: x[own] if node else x  # noqa: E731
+        hin = [sel(x, nd).cpu().pin_memory()
+               for x, nd in zip((Q, K, V, dO), (node_qk, node_qk, True, True))]
         hout = [torch.empty(x[own].shape, dtype=x.dtype).pin_memory() for x in (O, dQ, dK, dV)]
         h2d = sum(x.numel() * x.element_size() for x in hin)
         d2h = sum(x.numel() * x.element_size() for x in hout)
 
         def e2e_step():
-            for h, d in zip(hin, (Q, K, V, dO)):
-                d[own].copy_(h, non_blocking=True)
+            for h, d, nd in zip(hin, (Q, K, V, dO), (node_qk, node_qk, True, True)):
+                sel(d, nd).copy_(h, non_blocking=True)
             step()
             for h, d in zip(hout, (O, dQ, dK, dV)):
                 h.copy_(d[own], non_blocking=True)
@@ -1377,11 +1429,12 @@ def run_ours(args, cfg, rank, world, full=True):
     nb = (shard.hi - shard.lo) if sharded else n
     e_of = {"fwd": dg.e, "bwd_rows": dg.e,
             "bwd_cols": int(shard.csc_row.numel()) if sharded else dg.e}
-    ab = algorithmic_bytes(dom, layer, nb, e_of[dom], H, D)
+    ab = algorithmic_bytes(dom, layer, nb, e_of[dom], H, D, from_v=from_v)
     achieved = ab / (means[dom] / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = ncu_traffic(cfg, dom)
-    step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D) for k in means)
+    step_bytes = sum(algorithmic_bytes(k, layer, nb, e_of[k], H, D, from_v=from_v)
+                     for k in means)
     if not full:
         return {"workload": desc, "nodes": n, "edges": e, "value": value, "unit": "GEdges/s",
                 "ms_per_step": ms_per_step, "steps": steps,
@@ -1397,10 +1450,11 @@ def run_ours(args, cfg, rank, world, full=True):
                 "parallelism": (f"row-sharded x{world} (NCCL)" if sharded else "1 GPU")}
     l2_peak, l2_rb = measured_l2_gather(F * 4)
     a_ps, b_ps, g32, g128 = l2_request_costs()
-    req_model = {k: l2_request_model_ms(k, layer, H, D, e_of[k], a_ps, b_ps) for k in means}
+    req_model = {k: l2_request_model_ms(k, layer, H, D, e_of[k], a_ps, b_ps, from_v=from_v)
+                 for k in means}
     # node tables the dominant kernel gathers (fwd / pass A: V and Q|el; pass B:
     # dO, K (dot) and the records): the L2 denominator applies when they fit L2
-    gathered = {"fwd": F + qk, "bwd_rows": F + qk,
+    gathered = {"fwd": F + (0 if from_v else qk), "bwd_rows": F + (0 if from_v else qk),
                 "bwd_cols": F + (F if layer != "gat" else 0) + 4 * H}
     tables_bytes = 4 * n * gathered[dom]
 
@@ -1449,7 +1503,8 @@ def run_ours(args, cfg, rank, world, full=True):
                 m = fused.measure_metrics(fn, mets, prep=lambda: cold_l2(flush))
                 measured[k] = {"dram_bytes": m[mets[0]] + m[mets[1]],
                                "l2_to_l1_bytes": m[mets[2]],
-                               "algorithmic_bytes": algorithmic_bytes(k, layer, nb, e_of[k], H, D)}
+                               "algorithmic_bytes": algorithmic_bytes(k, layer, nb, e_of[k], H, D,
+                                                                      from_v=from_v)}
         except GFError as ex:  # no CUPTI / permission: the committed ncu file stands
             measured = {"error": str(ex)[:200]}
         if "error" not in measured:
@@ -1489,6 +1544,9 @@ def run_ours(args, cfg, rank, world, full=True):
                       "parallelism": (f"row-sharded x{world} (NCCL all-gather)" if sharded
                                       else "1 GPU")},
             "l2_carveout": carve,
+            "gat_form": ("layer: logits from the gathered V rows (GF_FLAG_LOGITS_FROM_V; Q, K = "
+                         "a_l, a_r)" if from_v else None),
+            "gat_table_form": table_form,
             "dropin_api": api,
             "measured_bytes": measured,
             "measured_bytes_note": ("per launch, cold L2 (persisting lines reset + 256 MiB "

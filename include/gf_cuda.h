@@ -54,6 +54,18 @@ extern "C" {
 #define GF_DOT 0 /* SddmmVariant::Dot (GT, AGNN) */
 #define GF_ADD 1 /* SddmmVariant::Add (GAT) */
 
+/* gf_attn_desc.reserved flags.
+ * GF_FLAG_LOGITS_FROM_V (GF_ADD only): the GAT layer's attention logits are
+ * linear in the projected features V = H (models.hpp:116-125): Q and K carry
+ * a_l and a_r (H x D, the layout of one V row, 32-byte aligned) and the
+ * kernels compute el[u,h] = <V[u,h,:], a_l[h,:]> from the V row they gather
+ * anyway and er[v,h] = <V[v,h,:], a_r[h,:]> from the destination's own row,
+ * instead of gathering an el table per edge.  Backward outputs are unchanged
+ * (dQ|del, dK|der are N x H).  Paths other than the fused fast kernels
+ * (strategies, P materialisation, generic shapes) compute el / er tables
+ * once (gf_gat_logits) and run the table form. */
+#define GF_FLAG_LOGITS_FROM_V 1
+
 /* Fusion strategies (reference Strategy enum, schedule.hpp:12-18). */
 #define GF_STRAT_SMMF 0     /* 1 launch, fused, nothing E x H in HBM (default)      */
 #define GF_STRAT_PMF 1      /* edge-parallel SDDMM -> S[E x H]; fused softmax+SpMM  */
@@ -69,7 +81,7 @@ typedef struct gf_attn_desc {
   int32_t l2;       /* AGNN: L2-normalise Q and K rows per head (dot only) */
   int32_t heads;    /* H >= 1 */
   int32_t head_dim; /* D >= 1 */
-  int32_t reserved;
+  int32_t reserved; /* flags (GF_FLAG_*); 0 = the reference's SddmmKind semantics */
   double scale;     /* dot only */
   double slope;     /* add only (LeakyReLU negative slope) */
 } gf_attn_desc;

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("GF_CUDA_LIB") or os.path.join(_HERE, "libgraphfuse_cu
 GF_OK = 0
 GF_F32, GF_F64 = 0, 1
 GF_DOT, GF_ADD = 0, 1
+GF_FLAG_LOGITS_FROM_V = 1  # gf_attn_desc.reserved flag (gf_cuda.h)
 GF_STRAT = {"smmf": 0, "pmf": 1, "unfused": 2, "baseline": 3}
 
 _vp = C.c_void_p

@@ -137,6 +137,12 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;
   const uint32_t fb = a.F * sizeof(T), qb = qs * sizeof(T);  // row strides in bytes
+  T al[NE];  // GF_ADDV: el = <V[u], a_l> from the gathered V row
+  if constexpr (VAR == GF_ADDV) {
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
+  }
 
   T dov[NE], kv[NE];
   T delta;
@@ -200,6 +206,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else if constexpr (VAR == GF_ADDV) {
+            el[t] = T(0);  // from the gathered V row below
           } else {
             el[t] = ld_node(row_at(Qb, uu, qb));
           }
@@ -225,6 +233,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
             }
             s = a.scale * d;
           } else {
+            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), a.LPH);
             pre = el[t] + erv;
             s = lrelu(pre, a.slope);
           }
@@ -276,6 +285,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else if constexpr (VAR == GF_ADDV) {
+            el[t] = T(0);  // from the gathered V row below
           } else {
             el[t] = ld_node(row_at(Qb, uu, qb));
           }
@@ -301,6 +312,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
             }
             s = a.scale * d;
           } else {
+            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), a.LPH);
             pre = el[t] + erv;
             s = lrelu(pre, a.slope);
           }
@@ -346,7 +358,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   }
   if (writer && c % a.LPH == 0) {
     a.stats[4 * ri + 3] = delta;
-    if constexpr (VAR == GF_ADD) a.dK[ri] = acc[0];
+    if constexpr (VAR != GF_DOT) a.dK[ri] = acc[0];
   }
   rs = rsn;
   rsn = rsnn;
@@ -426,6 +438,12 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
       for (int i = 0; i < NE; ++i) s += qu[i] * qu[i];
       rq = inv_norm(head_sum(s, a.LPH));
     }
+  } else if constexpr (VAR == GF_ADDV) {  // el = <V[u], a_l> from the owned V row
+    T al[NE];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
+    elu = head_sum(dot_n(vu, al), a.LPH);
   } else {
     elu = __ldg(a.Q + static_cast<size_t>(u) * a.H + h);
   }
@@ -608,7 +626,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
       if constexpr (VAR == GF_DOT)
         st_chunk<T, CB>(a.dQ + urow + k * CW, *reinterpret_cast<T(*)[CW]>(g + k * CW));
     }
-    if constexpr (VAR == GF_ADD) {
+    if constexpr (VAR != GF_DOT) {
       if (c % a.LPH == 0) a.dQ[static_cast<size_t>(u) * a.H + h] = all[NE];
     }
   }
@@ -819,6 +837,11 @@ int launch_fast_bwd(const BwdArgs<T>& ra, const BwdArgs<T>& ca, int variant, int
     GF_CHECK_LAUNCH("bwd_rows_fast");
     if (cblocks) bwd_cols_fast<T, CB, LPE, CPL, GF_DOT><<<cblocks, 256, 0, s>>>(ca);
     GF_CHECK_LAUNCH("bwd_cols_fast");
+  } else if (variant == GF_ADDV) {
+    if (rblocks) bwd_rows_fast<T, CB, LPE, CPL, GF_ADDV><<<rblocks, 256, 0, s>>>(ra);
+    GF_CHECK_LAUNCH("bwd_rows_fast");
+    if (cblocks) bwd_cols_fast<T, CB, LPE, CPL, GF_ADDV><<<cblocks, 256, 0, s>>>(ca);
+    GF_CHECK_LAUNCH("bwd_cols_fast");
   } else {
     if (rblocks) bwd_rows_fast<T, CB, LPE, CPL, GF_ADD><<<rblocks, 256, 0, s>>>(ra);
     GF_CHECK_LAUNCH("bwd_rows_fast");
@@ -859,10 +882,17 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   const int cb = fs.cb;
   const bool base = fs.ok && static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31) &&
                     aligned(a.stats, 32);
+  const bool addv = variant == GF_ADDV;
   const bool fast_a = base && aligned(a.V, cb) && aligned(a.O, 16) && aligned(a.dO, 16) &&
-                      (!dot || (aligned(a.Q, cb) && aligned(a.K, 16) && aligned(a.dK, 16)));
+                      (!dot || (aligned(a.Q, cb) && aligned(a.K, 16) && aligned(a.dK, 16))) &&
+                      (!addv || aligned(a.Q, cb));
   const bool fast_b = base && aligned(a.V, 16) && aligned(a.dO, cb) && aligned(a.dV, 16) &&
-                      (!dot || (aligned(a.Q, 16) && aligned(a.K, cb) && aligned(a.dQ, 16)));
+                      (!dot || (aligned(a.Q, 16) && aligned(a.K, cb) && aligned(a.dQ, 16))) &&
+                      (!addv || aligned(a.Q, cb));
+  if (addv && ((do_a && !fast_a) || (do_b && !fast_b))) {
+    set_error("gf_attn_bwd: logits-from-V needs the fast path (callers fall back to el/er tables)");
+    return GF_ERR_INVALID;
+  }
   ra.LPH = ca.LPH = fs.ok ? fs.lph : 1;
   // bucket geometry (see fwd): warp bucket [n_cta, pk0), packed [pk0, n)
   const int epw = fs.ok ? 32 / fs.lpe : 1;

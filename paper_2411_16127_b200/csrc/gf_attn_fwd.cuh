@@ -86,6 +86,12 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const T* __restrict__ Vb = a.V + off;
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
+  T al[NE];  // GF_ADDV: this lane's slice of a_l (el = <V[u], a_l> per head)
+  if constexpr (VAR == GF_ADDV) {
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
+  }
   const T* __restrict__ Sb = a.ES + h;        // MODE 1/2: ES[e * H + h]
 
   for (int r = 0; r < (GF_ROWPIPE ? nrows : 1); ++r) {
@@ -116,6 +122,15 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       rk = inv_norm(head_sum(s, a.LPH));
     }
     }
+  } else if constexpr (VAR == GF_ADDV) {  // er = <V[v], a_r> from the row's own V
+    T vo[NE], ar[NE];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      ld_own<T, CB>(a.V + static_cast<size_t>(v) * a.F + off + k * CW,
+                    *reinterpret_cast<T(*)[CW]>(vo + k * CW));
+      ld_own<T, CB>(a.K + off + k * CW, *reinterpret_cast<T(*)[CW]>(ar + k * CW));
+    }
+    erv = head_sum(dot_n(vo, ar), a.LPH);
   } else {
     erv = __ldg(a.K + static_cast<size_t>(v) * a.H + h);
   }
@@ -164,6 +179,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else if constexpr (VAR == GF_ADDV) {
+            // el from the gathered V row (after the slot loop)
           } else {
             s[t] = ld_node(Qb + uu * qs);
           }
@@ -191,6 +208,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
             s[t] = a.scale * d;
+          } else if constexpr (VAR == GF_ADDV) {
+            s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
           }
@@ -257,6 +276,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+          } else if constexpr (VAR == GF_ADDV) {
+            // el from the gathered V row (after the slot loop)
           } else {
             s[t] = ld_node(Qb + uu * qs);
           }
@@ -284,6 +305,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
             s[t] = a.scale * d;
+          } else if constexpr (VAR == GF_ADDV) {
+            s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
           }
@@ -535,6 +558,8 @@ int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cuda
     fwd_fast<T, CB, LPE, CPL, GF_ADD, 1><<<blocks, 256, 0, s>>>(a);
   else if (variant == GF_DOT)
     fwd_fast<T, CB, LPE, CPL, GF_DOT><<<blocks, 256, 0, s>>>(a);
+  else if (variant == GF_ADDV)
+    fwd_fast<T, CB, LPE, CPL, GF_ADDV><<<blocks, 256, 0, s>>>(a);
   else
     fwd_fast<T, CB, LPE, CPL, GF_ADD><<<blocks, 256, 0, s>>>(a);
   GF_CHECK_LAUNCH("fwd_fast");
@@ -602,7 +627,13 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
   const bool small = static_cast<int64_t>(g.n) * a.F < (int64_t(1) << 31);  // 32-bit row offsets
   const bool al = fs.ok && small && aligned(a.V, fs.cb) && aligned(a.O, 16) &&
                   aligned(a.stats, 32) &&
-                  (mode >= 2 || variant == GF_ADD || (aligned(a.Q, fs.cb) && aligned(a.K, 16)));
+                  (mode >= 2 || variant == GF_ADD ||
+                   (variant == GF_ADDV && aligned(a.Q, fs.cb) && aligned(a.K, fs.cb)) ||
+                   (variant == GF_DOT && aligned(a.Q, fs.cb) && aligned(a.K, 16)));
+  if (variant == GF_ADDV && (!al || mode != 0)) {
+    set_error("gf_attn_fwd: logits-from-V needs the fast path (callers fall back to el/er tables)");
+    return GF_ERR_INVALID;
+  }
   if (al) {
     a.LPH = fs.lph;
     const int epw = 32 / fs.lpe;

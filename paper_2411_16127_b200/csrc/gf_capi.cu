@@ -1,4 +1,5 @@
 #include <atomic>
+#include <initializer_list>
 #include <algorithm>
 #include <mutex>
 #include <cstdlib>
@@ -124,6 +125,56 @@ int check_desc(const gf_attn_desc* d, const char* who) {
     gfb::set_error(std::string(who) + ": invalid descriptor (dtype/variant/heads/head_dim/l2)");
     return GF_ERR_INVALID;
   }
+  if ((d->reserved & ~GF_FLAG_LOGITS_FROM_V) != 0 ||
+      ((d->reserved & GF_FLAG_LOGITS_FROM_V) && d->variant != GF_ADD)) {
+    gfb::set_error(std::string(who) + ": invalid descriptor flags (GF_FLAG_LOGITS_FROM_V needs GF_ADD)");
+    return GF_ERR_INVALID;
+  }
+  return GF_OK;
+}
+
+// GF_FLAG_LOGITS_FROM_V resolution for one call: the fused fast kernels take
+// a_l / a_r directly (kernel variant GF_ADDV); every other path gets el / er
+// tables computed once (gf_gat_logits) into stream-ordered scratch and runs
+// the table form.  Without the flag: pass-through.
+struct Logits {
+  int variant = GF_ADD;
+  const void* Q = nullptr;
+  const void* K = nullptr;
+  void* tables = nullptr;
+  cudaStream_t s = nullptr;
+  Logits() = default;
+  Logits(const Logits&) = delete;
+  ~Logits() {
+    if (tables) cudaFreeAsync(tables, s);
+  }
+};
+
+int resolve_logits(const gf_graph_s* g, const gf_attn_desc& d, const void* Q, const void* K,
+                   const void* V, bool fast_path, std::initializer_list<const void*> vec_ptrs,
+                   cudaStream_t s, Logits& out) {
+  out.variant = d.variant;
+  out.Q = Q;
+  out.K = K;
+  out.s = s;
+  if (!(d.reserved & GF_FLAG_LOGITS_FROM_V)) return GF_OK;
+  const int elem = d.dtype == GF_F32 ? 4 : 8;
+  const int64_t F = static_cast<int64_t>(d.heads) * d.head_dim;
+  bool fast = fast_path && gfb::fast_shape(d.heads, d.head_dim, elem, g->e).ok &&
+              static_cast<int64_t>(g->n) * F < (int64_t(1) << 31);
+  for (const void* p : vec_ptrs) fast = fast && (reinterpret_cast<uintptr_t>(p) % 32) == 0;
+  fast = fast && (reinterpret_cast<uintptr_t>(Q) % 32) == 0 && (reinterpret_cast<uintptr_t>(K) % 32) == 0;
+  if (fast) {
+    out.variant = gfb::GF_ADDV;
+    return GF_OK;
+  }
+  const size_t nb = static_cast<size_t>(g->n) * d.heads * elem;
+  GF_CHECK_CUDA(gfb::scratch_alloc_raw(&out.tables, 2 * nb + 64, s));
+  char* el = static_cast<char*>(out.tables);
+  char* er = el + (nb + 31) / 32 * 32;
+  if (int rc = gf_gat_logits(d.dtype, g->n, d.heads, d.head_dim, V, Q, K, el, er, s)) return rc;
+  out.Q = el;
+  out.K = er;
   return GF_OK;
 }
 
@@ -161,10 +212,12 @@ gfb::FwdArgs<T> fwd_args(const gfb::DevGraph& g, const gf_attn_desc& d, const vo
 template <typename T>
 int fwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, const void* V,
              void* O, void* lse, void* P, cudaStream_t s) {
-  auto a = fwd_args<T>(*g, d, Q, K, V, O, lse);
-  int rc = gfb::launch_fwd<T>(*g, a, d.variant, s);
+  Logits lg;  // P materialisation reads el / er tables
+  if (int rc = resolve_logits(g, d, Q, K, V, P == nullptr, {V, O, lse}, s, lg)) return rc;
+  auto a = fwd_args<T>(*g, d, lg.Q, lg.K, V, O, lse);
+  int rc = gfb::launch_fwd<T>(*g, a, lg.variant, s);
   if (rc || !P) return rc;
-  return gfb::launch_materialize_p<T>(*g, a, d.variant, static_cast<T*>(P), s);
+  return gfb::launch_materialize_p<T>(*g, a, lg.variant, static_cast<T*>(P), s);
 }
 
 template <typename T>
@@ -189,7 +242,11 @@ int bwd_impl(gf_graph_t g, const gf_attn_desc& d, const void* Q, const void* K, 
   a.dQ = static_cast<T*>(dQ);
   a.dK = static_cast<T*>(dK);
   a.dV = static_cast<T*>(dV);
-  return gfb::launch_bwd<T>(*g, a, d.variant, passes, s);
+  Logits lg;
+  if (int rc = resolve_logits(g, d, Q, K, V, true, {V, O, dO, dV, dK, dQ, stats}, s, lg)) return rc;
+  a.Q = static_cast<const T*>(lg.Q);
+  a.K = static_cast<const T*>(lg.K);
+  return gfb::launch_bwd<T>(*g, a, lg.variant, passes, s);
 }
 
 bool bad_graph(gf_graph_t g, const char* who) {
@@ -307,13 +364,19 @@ extern "C" int gf_attn_fwd_strategy(gf_graph_t g, const gf_attn_desc* desc, int3
     return GF_ERR_INVALID;
   }
   int rc;
+  Logits lg;
+  if ((rc = resolve_logits(g, *desc, Q, K, V, strategy == GF_STRAT_SMMF && !P, {V, O, stats}, s,
+                           lg))) {
+    if (own) cudaFreeAsync(ws, s);
+    return rc;
+  }
   if (desc->dtype == GF_F32)
-    rc = gfb::launch_fwd_strategy<float>(*g, fwd_args<float>(*g, *desc, Q, K, V, O, stats),
-                                         desc->variant, strategy, static_cast<float*>(P),
+    rc = gfb::launch_fwd_strategy<float>(*g, fwd_args<float>(*g, *desc, lg.Q, lg.K, V, O, stats),
+                                         lg.variant, strategy, static_cast<float*>(P),
                                          static_cast<float*>(ws), s);
   else
-    rc = gfb::launch_fwd_strategy<double>(*g, fwd_args<double>(*g, *desc, Q, K, V, O, stats),
-                                          desc->variant, strategy, static_cast<double*>(P),
+    rc = gfb::launch_fwd_strategy<double>(*g, fwd_args<double>(*g, *desc, lg.Q, lg.K, V, O, stats),
+                                          lg.variant, strategy, static_cast<double*>(P),
                                           static_cast<double*>(ws), s);
   if (own) cudaFreeAsync(ws, s);
   return rc;

@@ -8,6 +8,13 @@
 namespace gfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+template <typename T, int N>
+__device__ __forceinline__ T dot_n(const T (&x)[N], const T (&y)[N]) {
+  T s = T(0);
+#pragma unroll
+  for (int i = 0; i < N; ++i) s += x[i] * y[i];
+  return s;
+}
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ---------------------------------------------------------------- chunks --

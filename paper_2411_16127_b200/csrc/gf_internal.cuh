@@ -13,6 +13,13 @@
 
 namespace gfb {
 
+// Kernel variant of the GAT layer (gf_attn_desc flag GF_FLAG_LOGITS_FROM_V):
+// additive scores whose logits are linear in the gathered V row itself,
+// el[u,h] = <V[u,h,:], a_l[h,:]>, er[v,h] = <V[v,h,:], a_r[h,:]> (models.hpp:
+// 116-125, V = H), so no el table is gathered per edge.  Q / K carry a_l / a_r
+// (H x D, the layout of a V row).  Internal: not a gf_attn_desc.variant value.
+constexpr int GF_ADDV = 2;
+
 // ------------------------------------------------------------------ errors --
 void set_error(const std::string& msg);
 

@@ -279,8 +279,9 @@ int sddmm_backward_impl(DevGraph& g, const gf_attn_desc& d, const T* Q, const T*
 int check_desc(const gf_attn_desc* d, const char* who) {
   if (!d || (d->dtype != GF_F32 && d->dtype != GF_F64) ||
       (d->variant != GF_DOT && d->variant != GF_ADD) || d->heads < 1 || d->head_dim < 1 ||
-      (d->variant == GF_ADD && d->l2)) {
-    set_error(std::string(who) + ": invalid descriptor");
+      (d->variant == GF_ADD && d->l2) || d->reserved != 0) {
+    set_error(std::string(who) + ": invalid descriptor (the single-step ops take explicit "
+              "el / er: no descriptor flags)");
     return GF_ERR_INVALID;
   }
   return GF_OK;

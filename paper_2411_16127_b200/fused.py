@@ -6,6 +6,8 @@ call into libgraphfuse_cuda.so.  Layout (see include/gf_cuda.h):
 """
 from __future__ import annotations
 
+import dataclasses
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -37,11 +39,17 @@ class AttnSpec:
     scale: float = 1.0
     slope: float = 0.2
     l2: bool = False
+    # GAT layer form (GF_FLAG_LOGITS_FROM_V): Q / K are a_l / a_r (H x D, one
+    # V row's layout) and el / er are computed from V's rows in the kernels
+    logits_from_v: bool = False
 
     def desc(self, dtype) -> AttnDesc:
+        if self.logits_from_v and self.variant != "add":
+            raise ValueError("logits_from_v needs variant='add'")
         return AttnDesc(DTYPES[dtype], _capi.GF_ADD if self.variant == "add" else _capi.GF_DOT,
-                        int(self.l2), self.heads, self.head_dim, 0, float(self.scale),
-                        float(self.slope))
+                        int(self.l2), self.heads, self.head_dim,
+                        _capi.GF_FLAG_LOGITS_FROM_V if self.logits_from_v else 0,
+                        float(self.scale), float(self.slope))
 
     @property
     def F(self) -> int:
@@ -380,6 +388,9 @@ def attn_backward_unfused(g: DeviceGraph, spec: AttnSpec, Q, K, V, P, dO, stream
     """The reference's unfused backward (autograd.hpp:158-170, 196-203): dP/dV,
     then dS, then dQ/dK, with the E x H edge gradients in HBM.  Returns
     (dQ|del, dK|der, dV, dP, dS)."""
+    if spec.logits_from_v:  # the single-step ops take explicit el / er tables
+        Q, K = gat_logits(V, Q, K, spec.heads, spec.head_dim, stream=stream)
+        spec = dataclasses.replace(spec, logits_from_v=False)
     dP, dV = spmm_backward(g, spec.heads, spec.head_dim, P, V, dO, stream=stream)
     dS = softmax_backward(g, spec.heads, P, dP, stream=stream)
     dQ, dK = sddmm_backward(g, spec, Q, K, dS, stream=stream)

@@ -40,3 +40,13 @@ def test_algorithmic_bytes_c4():
     assert got["fwd"] == pytest.approx(33.4, abs=0.1)
     assert got["bwd_rows"] == pytest.approx(33.5, abs=0.1)
     assert got["bwd_cols"] == pytest.approx(44.5, abs=0.1)
+
+
+def test_layer_form_models():
+    """GAT layer form (GF_FLAG_LOGITS_FROM_V): no el gather in fwd / pass A."""
+    assert bench.gathered_rows("fwd", "gat", 8, 8, from_v=True) == [256]
+    assert bench.gathered_rows("bwd_rows", "gat", 8, 8, from_v=True) == [256]
+    assert bench.gathered_rows("bwd_cols", "gat", 8, 8, from_v=True) == [256, 128]
+    full = bench.algorithmic_bytes("fwd", "gat", N4, E4, 8, 8)
+    lay = bench.algorithmic_bytes("fwd", "gat", N4, E4, 8, 8, from_v=True)
+    assert full - lay == 4 * E4 * 8 - 4 * N4 * (64 - 8)  # el per edge gone; own V row per node
