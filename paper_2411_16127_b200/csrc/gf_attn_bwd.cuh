@@ -111,12 +111,14 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const int c = lane % LPE, sub = lane / LPE;
   // nrows consecutive warp rows, software-pipelined like fwd_row (gf_attn_fwd.cuh)
   const int4 zero4 = make_int4(0, 0, 0, 0);
-#if GF_SCHED16_ROWS
-  int4 rs = live ? ld_sched(a.sched + slot) : zero4;
-#else
-  const int v0 = live ? __ldg(a.order + slot) : 0;
-  int4 rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
-#endif
+  constexpr bool PKPRE = PK && LPE >= kSmallDegree;  // packed rows: ids loaded up front
+  int4 rs;
+  if constexpr (GF_SCHED16_ROWS || PK) {
+    rs = live ? ld_sched(a.sched + slot) : zero4;
+  } else {
+    const int v0 = live ? __ldg(a.order + slot) : 0;
+    rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
+  }
   int4 rsn = nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
   int nxt = 0;
   for (int r = 0; r < nrows; ++r) {
@@ -128,6 +130,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
     split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
   }
   if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
+  if constexpr (PKPRE) nxt = c < ee - eb ? ld_idx(a.idx + eb + c) : 0;
 
   const int h = c / a.LPH;
   const int off = h * a.D + (c % a.LPH) * NE;
@@ -197,7 +200,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
-          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
           const int uu = ok[t] ? u : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
@@ -276,7 +280,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
-          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
           const int uu = ok[t] ? u : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
@@ -407,8 +412,15 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   const int c = lane % LPE, sub = lane / LPE;
   // No row pipelining / 16 B schedule entries here: at pass B's 64-register
   // budget (4 CTAs/SM) either spills; the launcher keeps rpw = 1.
-  const int u = live ? __ldg(a.order + slot) : 0;
-  int sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
+  constexpr bool PKPRE = PK && LPE >= kSmallDegree;  // packed columns: sched entry + ids up front
+  int u, sb, se;
+  if constexpr (PK) {
+    const int4 e = live ? ld_sched(a.sched + slot) : make_int4(0, 0, 0, 0);
+    u = e.x, sb = e.y, se = e.z;
+  } else {
+    u = live ? __ldg(a.order + slot) : 0;
+    sb = live ? __ldg(a.ptr + u) : 0, se = live ? __ldg(a.ptr + u + 1) : 0;
+  }
   if (cta) {
     if (ct.z > 1) split_range(sb, se, ct.z, ct.y, sb, se);  // this CTA's slice of a split column
     split_range(sb, se, kWarpsPerBlock, warp, sb, se);
@@ -455,6 +467,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   constexpr int ep = pk ? 1 : EPW;
   const int js = pk ? 0 : sub;
   int nxt = !pk && sb + lane < se ? ld_idx(a.idx + sb + lane) : 0;
+  if constexpr (PKPRE) nxt = c < se - sb ? ld_idx(a.idx + sb + c) : 0;
   for (int base = sb; pk || base < se; base += 32) {
     const int cnt = pk ? se - sb : min(32, se - base);
     const int cntw = pk ? static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt))) : cnt;
@@ -473,7 +486,8 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
-          const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
+          const int v = PKPRE ? __shfl_sync(kFull, myv, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
           const int vv = ok[t] ? v : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
@@ -548,7 +562,8 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
-          const int v = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
+          const int v = PKPRE ? __shfl_sync(kFull, myv, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myv, j & 31);
           const int vv = ok[t] ? v : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)

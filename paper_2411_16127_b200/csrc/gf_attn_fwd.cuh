@@ -72,12 +72,17 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
   const int4 zero4 = make_int4(0, 0, 0, 0);
-#if GF_SCHED16_FWD
-  int4 rs = live ? ld_sched(a.sched + slot) : zero4;
-#else
-  const int v0 = live ? __ldg(a.order + slot) : 0;
-  int4 rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
-#endif
+  // Packed rows (degree <= kSmallDegree): the 16 B schedule entry (one load
+  // instead of order -> pointers), and each lane group loads its row's ids
+  // once up front (one id per lane) instead of one dependent load per edge.
+  constexpr bool PKPRE = PK && LPE >= kSmallDegree;
+  int4 rs;
+  if constexpr (GF_SCHED16_FWD || PK) {
+    rs = live ? ld_sched(a.sched + slot) : zero4;
+  } else {
+    const int v0 = live ? __ldg(a.order + slot) : 0;
+    rs = live ? make_int4(v0, __ldg(a.ptr + v0), __ldg(a.ptr + v0 + 1), 0) : zero4;
+  }
   int4 rsn = GF_ROWPIPE && nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
   int nxt = 0;
 
@@ -103,6 +108,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
     split_range(eb, ee, kWarpsPerBlock, warp, eb, ee);
   }
   if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
+  if constexpr (PKPRE) nxt = c < ee - eb ? ld_idx(a.idx + eb + c) : 0;
 
   // Destination-side operands stay in registers for the whole row.
   T kv[NE];
@@ -166,7 +172,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
-          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
           const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
@@ -263,7 +270,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
-          const int u = pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
+          const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
+                        : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
           const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
