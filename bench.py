@@ -1188,8 +1188,17 @@ def run_ours(args, cfg, rank, world, full=True):
             O_parts, rec_parts = shard_mod.part_buffers(parts, spec, device=dev)
             order = shard_mod.phase_order(shard)
 
-    def step(ev=None):
-        rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
+    def step(ev=None, ends_only=False):
+        # ends_only: events at the step's start and end only, so the kernels
+        # follow each other back to back (programmatic dependent launch can
+        # overlap a launch with the previous kernel's tail); the per-kernel
+        # breakdown comes from a separate loop with an event between kernels.
+        if not ev:
+            rec = lambda i: None  # noqa: E731
+        elif ends_only:
+            rec = lambda i: ev[i].record(stream) if i in (0, NEV - 1) else None  # noqa: E731
+        else:
+            rec = lambda i: ev[i].record(stream)  # noqa: E731
         k = 0
         rec(k)
         later = []
@@ -1237,14 +1246,14 @@ def run_ours(args, cfg, rank, world, full=True):
         k += 1
         rec(k)
 
-    def timed(nsteps):
+    def timed(nsteps, ends_only=True):
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NEV)] for _ in range(nsteps)]
         if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for i in range(nsteps):
             cold_l2(flush)  # the flush runs while the host enqueues the step: no launch gap
-            step(evs[i])
+            step(evs[i], ends_only=ends_only)
         torch.cuda.synchronize()
         if sharded:
             torch.distributed.barrier()
@@ -1257,7 +1266,9 @@ def run_ours(args, cfg, rank, world, full=True):
     with ClockSampler(local) as clk:
         clk.wait_first()
         evs = timed(steps)
-    seg = [[a[j].elapsed_time(a[j + 1]) for a in evs] for j in range(NEV - 1)]
+    # per-kernel breakdown: the same step with an event between kernels
+    evs_k = timed(max(5, min(steps, 20)), ends_only=False)
+    seg = [[a[j].elapsed_time(a[j + 1]) for a in evs_k] for j in range(NEV - 1)]
     if sharded:
         k_ag1, k_fwd, k_ra, k_ag2, k_rb = seg
     else:
@@ -1285,7 +1296,8 @@ def run_ours(args, cfg, rank, world, full=True):
         for _ in range(2):
             step()
         ms_t = whole_job_ms(timed(steps))
-        kt = {nm: round(statistics.mean(a[j].elapsed_time(a[j + 1]) for a in timed(5)), 4)
+        ek = timed(5, ends_only=False)
+        kt = {nm: round(statistics.mean(a[j].elapsed_time(a[j + 1]) for a in ek), 4)
               for j, nm in enumerate(("fwd", "bwd_rows", "bwd_cols"))}
         Q, K, spec = Qs, Ks, spec_l
         del EL, ER

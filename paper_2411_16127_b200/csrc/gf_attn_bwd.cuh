@@ -394,6 +394,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
+  pdl_launch();
+  pdl_wait();
   GF_BWD_DISPATCH(bwd_row)
 }
 
@@ -651,6 +653,8 @@ template <typename T, int CB, int LPE, int CPL, int VAR>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
   // one call site for CTA and warp columns (runtime `cta`): two inlined copies
   // push pass B past its 64-register budget
+  pdl_launch();
+  pdl_wait();
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cb = a.cta_tab ? a.cta_blocks : a.n_cta;
@@ -848,19 +852,19 @@ template <typename T, int CB, int LPE, int CPL>
 int launch_fast_bwd(const BwdArgs<T>& ra, const BwdArgs<T>& ca, int variant, int rblocks,
                     int cblocks, cudaStream_t s) {
   if (variant == GF_DOT) {
-    if (rblocks) bwd_rows_fast<T, CB, LPE, CPL, GF_DOT><<<rblocks, 256, 0, s>>>(ra);
+    if (rblocks) GF_CHECK_CUDA(launch_k(bwd_rows_fast<T, CB, LPE, CPL, GF_DOT>, rblocks, 256, s, ra));
     GF_CHECK_LAUNCH("bwd_rows_fast");
-    if (cblocks) bwd_cols_fast<T, CB, LPE, CPL, GF_DOT><<<cblocks, 256, 0, s>>>(ca);
+    if (cblocks) GF_CHECK_CUDA(launch_k(bwd_cols_fast<T, CB, LPE, CPL, GF_DOT>, cblocks, 256, s, ca));
     GF_CHECK_LAUNCH("bwd_cols_fast");
   } else if (variant == GF_ADDV) {
-    if (rblocks) bwd_rows_fast<T, CB, LPE, CPL, GF_ADDV><<<rblocks, 256, 0, s>>>(ra);
+    if (rblocks) GF_CHECK_CUDA(launch_k(bwd_rows_fast<T, CB, LPE, CPL, GF_ADDV>, rblocks, 256, s, ra));
     GF_CHECK_LAUNCH("bwd_rows_fast");
-    if (cblocks) bwd_cols_fast<T, CB, LPE, CPL, GF_ADDV><<<cblocks, 256, 0, s>>>(ca);
+    if (cblocks) GF_CHECK_CUDA(launch_k(bwd_cols_fast<T, CB, LPE, CPL, GF_ADDV>, cblocks, 256, s, ca));
     GF_CHECK_LAUNCH("bwd_cols_fast");
   } else {
-    if (rblocks) bwd_rows_fast<T, CB, LPE, CPL, GF_ADD><<<rblocks, 256, 0, s>>>(ra);
+    if (rblocks) GF_CHECK_CUDA(launch_k(bwd_rows_fast<T, CB, LPE, CPL, GF_ADD>, rblocks, 256, s, ra));
     GF_CHECK_LAUNCH("bwd_rows_fast");
-    if (cblocks) bwd_cols_fast<T, CB, LPE, CPL, GF_ADD><<<cblocks, 256, 0, s>>>(ca);
+    if (cblocks) GF_CHECK_CUDA(launch_k(bwd_cols_fast<T, CB, LPE, CPL, GF_ADD>, cblocks, 256, s, ca));
     GF_CHECK_LAUNCH("bwd_cols_fast");
   }
   return GF_OK;

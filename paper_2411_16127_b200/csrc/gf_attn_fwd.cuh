@@ -444,6 +444,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
 // warp, one LPE-lane group each); the bucket is warp-uniform.
 template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
 __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
+  pdl_launch();
+  pdl_wait();
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cb = a.cta_tab ? a.cta_blocks : a.n_cta;  // CTA-bucket blocks
@@ -557,19 +559,19 @@ __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __re
 template <typename T, int CB, int LPE, int CPL>
 int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cudaStream_t s) {
   if (mode == 2)  // edge weights given: the score variant is irrelevant
-    fwd_fast<T, CB, LPE, CPL, GF_ADD, 2><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADD, 2>, blocks, 256, s, a));
   else if (mode == 3)
-    fwd_fast<T, CB, LPE, CPL, GF_ADD, 3><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADD, 3>, blocks, 256, s, a));
   else if (mode == 1 && variant == GF_DOT)
-    fwd_fast<T, CB, LPE, CPL, GF_DOT, 1><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_DOT, 1>, blocks, 256, s, a));
   else if (mode == 1)
-    fwd_fast<T, CB, LPE, CPL, GF_ADD, 1><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADD, 1>, blocks, 256, s, a));
   else if (variant == GF_DOT)
-    fwd_fast<T, CB, LPE, CPL, GF_DOT><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_DOT>, blocks, 256, s, a));
   else if (variant == GF_ADDV)
-    fwd_fast<T, CB, LPE, CPL, GF_ADDV><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADDV>, blocks, 256, s, a));
   else
-    fwd_fast<T, CB, LPE, CPL, GF_ADD><<<blocks, 256, 0, s>>>(a);
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADD>, blocks, 256, s, a));
   GF_CHECK_LAUNCH("fwd_fast");
   return GF_OK;
 }

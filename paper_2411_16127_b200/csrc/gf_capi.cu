@@ -52,6 +52,16 @@ cudaMemPool_t scratch_pool(int dev) { return dev >= 0 && dev < 64 ? pools[dev] :
 }  // namespace gfb
 
 
+namespace gfb {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GF_PDL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+}  // namespace gfb
+
 extern "C" int gf_scratch_trim(void) {
   int dev = 0;
   GF_CHECK_CUDA(cudaGetDevice(&dev));

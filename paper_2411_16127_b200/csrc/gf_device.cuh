@@ -8,6 +8,11 @@
 namespace gfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+// PDL (gf_internal.cuh launch_k): wait for the previous grid's completion and
+// memory before touching global memory; let the next grid be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 template <typename T, int N>
 __device__ __forceinline__ T dot_n(const T (&x)[N], const T (&y)[N]) {
   T s = T(0);

@@ -165,6 +165,29 @@ inline int rows_per_warp(int64_t edges, int64_t nodes, int64_t warp_rows) {
   return r >= 8 ? 8 : r >= 4 ? 4 : r >= 2 ? 2 : 1;
 }
 constexpr int kWarpsPerBlock = 8;  // 256-thread CTAs for every attention kernel
+
+// Programmatic dependent launch (PDL) for the attention kernels: launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, a kernel's CTAs may be
+// scheduled while the previous kernel in the stream is still finishing; every
+// fast kernel executes griddepcontrol.wait (pdl_wait) before its first global
+// memory access, so it still observes all of the previous kernel's writes,
+// and pdl_launch lets the next kernel be scheduled early.  Hides the launch
+// latency between fwd -> pass A -> pass B (small graphs).  GF_PDL=0 disables.
+bool pdl_enabled();
+template <typename Kern, typename Arg>
+cudaError_t launch_k(Kern k, int blocks, int threads, cudaStream_t s, const Arg& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
 // Edges per CTA slice of a split row: no CTA of a pass holds more than ~1/4
 // of one SM's share of the edges (148 SMs), and never fewer than a CTA row.
 // GF_SPLIT_LEN=<edges> overrides (A/B; a huge value disables splitting).
