@@ -105,7 +105,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? GF_U_ROWS : GF_U2;
+  constexpr int U = CPL == 1 ? GF_U_ROWS : (PK ? GF_U2_PK : GF_U2);
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
@@ -408,7 +408,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? GF_U_COLS : GF_U2;
+  constexpr int U = CPL == 1 ? GF_U_COLS : (PK ? GF_U2_PK : GF_U2);
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
   constexpr bool pk = PK;  // packed column: this LPE-lane group owns the column
   const int c = lane % LPE, sub = lane / LPE;

@@ -143,6 +143,9 @@ struct DevGraph {
 #ifndef GF_U2
 #define GF_U2 1
 #endif
+#ifndef GF_U2_PK
+#define GF_U2_PK 1  // packed rows of two-chunk lanes (A/B knob)
+#endif
 
 constexpr int kDefaultCtaThreshold = 1024;  // floor of the automatic threshold
 // Automatic CTA-row threshold: a row gets a whole CTA once it holds more than
