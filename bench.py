@@ -589,6 +589,9 @@ def main(argv=None):
                          "epilogue into symmetric memory (p2p) or by NCCL all-gather")
     ap.add_argument("--phased", choices=("auto", "on", "off"), default="auto",
                     help="sharded step: source-phased forward overlapping the source-row exchange")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: ranks may share a GPU (a flow check of the sharded step on a "
+                         "1-GPU box; not a scaling measurement)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the row-sharded path (NCCL all-gathers) even at N=1")
     args = ap.parse_args(argv)
@@ -609,6 +612,9 @@ def main(argv=None):
     from paper_2411_16127_b200._capi import check, lib
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":  # flow check: ranks may share the box's GPUs
+        local %= max(1, torch.cuda.device_count())
+    os.environ["GF_LOCAL_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or args.force_shard:
@@ -618,7 +624,10 @@ def main(argv=None):
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     # opt-in persisting-L2 set-aside (the library never changes it by itself)
     check(lib().gf_l2_persist(max(0, args.l2_persist_mib) << 20), "gf_l2_persist")
     out = run_ours(args, args.config, rank, world, full=True)
@@ -778,8 +787,8 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
     # symmetric memory, device barrier); "nccl" = projection, then all-gather.
     pt, exchange = None, None
     if shard is not None:
-        exchange = "nccl"
-        if getattr(args, "exchange", "p2p") == "p2p":
+        exchange = args.dist_backend  # all-gather over the process group
+        if getattr(args, "exchange", "p2p") == "p2p" and args.dist_backend == "nccl":
             try:
                 from paper_2411_16127_b200.shard import PeerTables
 
@@ -841,7 +850,8 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
             q, k, v = Qb, Kb, Hf
         if shard is not None and pt is None:  # source rows first; dO (and K) under fwd / pass A
-            for w in [all_gather_rows(t, shard, async_op=True) for t in (v, q)]:
+            for w in [all_gather_rows(t, shard, async_op=True)
+                      for t in (v,) + (() if spec.logits_from_v else (q,))]:
                 w.wait()
             later = [all_gather_rows(t, shard, async_op=True)
                      for t in (dO,) + (() if gat else (k,))]
@@ -1101,7 +1111,7 @@ def run_ours(args, cfg, rank, world, full=True):
     from paper_2411_16127_b200._capi import check, lib
 
     graph, layer, H, D, desc = CONFIGS[cfg]
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("GF_LOCAL_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     dev = torch.device("cuda", local)
     sharded = world > 1 or args.force_shard
     steps = args.steps if full else max(3, min(args.steps, 10))
@@ -1544,7 +1554,9 @@ def run_ours(args, cfg, rank, world, full=True):
         info = dg.info
         out = {
             "metric": "fused AT-GNN layer fwd+bwd GEdges/s", "value": value, "unit": "GEdges/s",
-            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "n_gpus": (world if args.dist_backend == "nccl"
+                       else min(world, max(1, torch.cuda.device_count()))),
+            "ranks": world, "dist_backend": args.dist_backend if sharded else None,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_key(cfg),
