@@ -1557,6 +1557,7 @@ def run_ours(args, cfg, rank, world, full=True):
             "n_gpus": (world if args.dist_backend == "nccl"
                        else min(world, max(1, torch.cuda.device_count()))),
             "ranks": world, "dist_backend": args.dist_backend if sharded else None,
+            "steps": steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_key(cfg),
