@@ -105,7 +105,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? GF_U_ROWS : (PK ? GF_U2_PK : GF_U2);
+  constexpr int U = CPL == 1 ? (VAR == GF_ADDV ? GF_U_ROWS_V : GF_U_ROWS) : (PK ? GF_U2_PK : GF_U2);
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;

@@ -68,7 +68,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? GF_U_FWD : (PK ? GF_U2_PK : GF_U2);
+  constexpr int U = CPL == 1 ? (VAR == GF_ADDV ? GF_U_FWD_V : GF_U_FWD) : (PK ? GF_U2_PK : GF_U2);
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
   const int4 zero4 = make_int4(0, 0, 0, 0);

@@ -143,6 +143,12 @@ struct DevGraph {
 #ifndef GF_U2
 #define GF_U2 1
 #endif
+#ifndef GF_U_FWD_V
+#define GF_U_FWD_V GF_U_FWD  // GAT layer form (GF_ADDV) forward
+#endif
+#ifndef GF_U_ROWS_V
+#define GF_U_ROWS_V GF_U_ROWS  // GAT layer form pass A
+#endif
 #ifndef GF_U2_PK
 #define GF_U2_PK 1  // packed rows of two-chunk lanes (A/B knob)
 #endif
