@@ -112,7 +112,10 @@ int gf_device_ok(void);
  * (the C++ host layer and the pybind module use only this C-ABI).
  * gf_malloc / gf_free are stream-ordered on the legacy default stream (the
  * library's private pool): use the buffer on that stream or on a blocking
- * stream.  kind: 0 host->device, 1 device->host, 2 device->device. */
+ * stream.  kind: 0 host->device, 1 device->host, 2 device->device.
+ * gf_memcpy of >= 64 MiB between pageable host memory and the device goes
+ * through a pinned staging ring (DMA of one chunk overlapping the host copy
+ * of the previous one) and returns when the copy is complete. */
 int gf_malloc(size_t bytes, void** out);
 int gf_free(void* p);
 int gf_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);

@@ -541,18 +541,32 @@ __global__ void __launch_bounds__(128) fwd_generic(const FwdArgs<T> a) {
 // P materialisation (reference ForwardContext::P, engine.hpp:29): recompute
 // p = exp(s - m - log l) per edge and head.  Only on explicit request.
 template <typename T, int VAR>
+// Warp per row; the per-head row operands (er | 1/||K||, the softmax record)
+// are staged in shared memory by lanes h < H, then all 32 lanes stride over
+// the row's (edge, head) pairs, so the E x H writes are coalesced and a
+// single-head call (the reference API is single-head) keeps every lane busy.
 __global__ void __launch_bounds__(128) materialize_p(const FwdArgs<T> a, T* __restrict__ P) {
+  __shared__ T s_er[kGenericWarps][32], s_rk[kGenericWarps][32];
+  __shared__ Rec<T> s_rec[kGenericWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int v = blockIdx.x * kGenericWarps + warp;
-  if (v >= a.n || lane >= a.H) return;
+  if (v >= a.n) return;  // warp-uniform
   const int eb = __ldg(a.ptr + v), ee = __ldg(a.ptr + v + 1);
-  T erh, rkh;
-  generic_row_setup<T, VAR>(a, v, lane, nullptr, erh, rkh);
-  const Rec<T> r = ld_rec(a.stats, static_cast<size_t>(v) * a.H + lane);
-  for (int i = eb; i < ee; ++i) {
+  if (lane < a.H) {
+    T erh, rkh;
+    generic_row_setup<T, VAR>(a, v, lane, nullptr, erh, rkh);
+    s_er[warp][lane] = erh;
+    s_rk[warp][lane] = rkh;
+    s_rec[warp][lane] = ld_rec(a.stats, static_cast<size_t>(v) * a.H + lane);
+  }
+  __syncwarp();
+  const int total = (ee - eb) * a.H;
+  for (int k = lane; k < total; k += 32) {
+    const int i = eb + k / a.H, h = k % a.H;
     const int u = __ldg(a.idx + i);
-    P[static_cast<size_t>(i) * a.H + lane] =
-        prob(generic_score<T, VAR>(a, u, v, lane, nullptr, erh, rkh), r);
+    P[static_cast<size_t>(i) * a.H + h] =
+        prob(generic_score<T, VAR>(a, u, v, h, nullptr, s_er[warp][h], s_rk[warp][h]),
+             s_rec[warp][h]);
   }
 }
 

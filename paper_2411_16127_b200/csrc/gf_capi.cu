@@ -1,4 +1,6 @@
 #include <atomic>
+#include <cstring>
+#include <thread>
 #include <initializer_list>
 #include <algorithm>
 #include <mutex>
@@ -102,12 +104,107 @@ extern "C" int gf_free(void* p) {
   return GF_OK;
 }
 
+namespace {
+// Large copies between PAGEABLE host memory and the device (the drop-in C++
+// API's std::vector operands, e.g. the E-length P of run_strategy) go through
+// a persistent pinned staging ring: the DMA of chunk i overlaps the host
+// memcpy of chunk i-1 (4 threads), instead of the driver's pageable path.
+constexpr size_t kStageChunk = size_t(32) << 20;
+constexpr size_t kStageMin = size_t(64) << 20;
+
+struct Stage {
+  std::mutex mu;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool ok = false;
+  bool init() {
+    if (ok) return true;
+    for (int i = 0; i < 2; ++i)
+      if (cudaHostAlloc(&buf[i], kStageChunk, cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+    ok = true;
+    return true;
+  }
+};
+
+Stage& stage() {
+  static Stage st;
+  return st;
+}
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+  constexpr int kThreads = 4;
+  if (n < (size_t(4) << 20)) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::thread th[kThreads - 1];
+  const size_t part = (n / kThreads + 63) / 64 * 64;
+  for (int t = 1; t < kThreads; ++t) {
+    const size_t b = std::min(n, part * t), e = std::min(n, part * (t + 1));
+    th[t - 1] = std::thread([=] {
+      if (e > b) std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+    });
+  }
+  std::memcpy(dst, src, std::min(n, part));
+  for (auto& x : th) x.join();
+}
+
+int staged_copy(void* dst, const void* src, size_t bytes, bool d2h, cudaStream_t s) {
+  Stage& st = stage();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (!st.init()) return -1;  // caller falls back to the plain copy
+  const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+  auto len = [&](size_t i) { return std::min(kStageChunk, bytes - i * kStageChunk); };
+  if (d2h) {
+    for (size_t i = 0; i <= nch; ++i) {
+      if (i < nch) {
+        GF_CHECK_CUDA(cudaMemcpyAsync(st.buf[i % 2], static_cast<const char*>(src) + i * kStageChunk,
+                                      len(i), cudaMemcpyDeviceToHost, s));
+        GF_CHECK_CUDA(cudaEventRecord(st.ev[i % 2], s));
+      }
+      if (i > 0) {  // chunk i-1 landed: copy it out while chunk i is in flight
+        GF_CHECK_CUDA(cudaEventSynchronize(st.ev[(i - 1) % 2]));
+        par_memcpy(static_cast<char*>(dst) + (i - 1) * kStageChunk, st.buf[(i - 1) % 2], len(i - 1));
+      }
+    }
+  } else {
+    for (size_t i = 0; i < nch; ++i) {
+      if (i >= 2) GF_CHECK_CUDA(cudaEventSynchronize(st.ev[i % 2]));  // buffer free again
+      par_memcpy(st.buf[i % 2], static_cast<const char*>(src) + i * kStageChunk, len(i));
+      GF_CHECK_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + i * kStageChunk, st.buf[i % 2], len(i),
+                                    cudaMemcpyHostToDevice, s));
+      GF_CHECK_CUDA(cudaEventRecord(st.ev[i % 2], s));
+    }
+    for (int b = 0; b < 2; ++b) GF_CHECK_CUDA(cudaEventSynchronize(st.ev[b]));
+  }
+  return GF_OK;
+}
+}  // namespace
+
 extern "C" int gf_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream) {
   if (bytes == 0) return GF_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  if ((kind == 0 || kind == 1) && bytes >= kStageMin && is_pageable(kind == 0 ? src : dst)) {
+    const int rc = staged_copy(dst, src, bytes, kind == 1, s);
+    if (rc >= 0) return rc;
+  }
   const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
                            : kind == 1 ? cudaMemcpyDeviceToHost
                                        : cudaMemcpyDeviceToDevice;
-  GF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)));
+  GF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, k, s));
   return GF_OK;
 }
 

@@ -246,9 +246,12 @@ double device_forward_dram_bytes(const Graph& g, const FusionPlan& plan, const D
   };
   const char* names[2] = {"dram__bytes_read.sum", "dram__bytes_write.sum"};
   double vals[2] = {0, 0};
-  const int rc = gf_measure_metrics(prep, run, &r, names, 2, vals);
-  if (rc == GF_ERR_UNSUPPORTED) return -1.0;
-  if (rc != GF_OK) device_fail("gf_measure_metrics");
+  // A counter session can fail transiently (e.g. the profiler being busy):
+  // retry once, and report the column as unavailable rather than failing the
+  // benchmark over a diagnostic.
+  int rc = gf_measure_metrics(prep, run, &r, names, 2, vals);
+  if (rc != GF_OK && rc != GF_ERR_UNSUPPORTED) rc = gf_measure_metrics(prep, run, &r, names, 2, vals);
+  if (rc != GF_OK) return -1.0;
   return vals[0] + vals[1];
 }
 template double device_forward_dram_bytes<float>(const Graph&, const FusionPlan&,

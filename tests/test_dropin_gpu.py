@@ -194,8 +194,11 @@ def test_run_benchmark_json(cuda, name):
                      "device_bandwidth_utilization,device_dram_bytes")
     assert all(float(r.split(",")[12]) > 0 for r in dl[1:])
     # measured DRAM bytes of each mode's forward (CUPTI), L2 flushed first: at
-    # least the gathered inputs' footprint is read from DRAM
-    assert all(int(r.split(",")[15]) > 0 for r in dl[1:]), dl
+    # least the gathered inputs' footprint is read from DRAM ("NA" only if a
+    # counter session failed)
+    col = [r.split(",")[15] for r in dl[1:]]
+    assert all(c == "NA" or int(c) > 0 for c in col), dl
+    assert sum(c != "NA" for c in col) >= max(1, len(col) - 1), dl
     assert "| mode |" in md
 
 
