@@ -393,7 +393,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   }
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_ROWS : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV ? GF_MINB_ROWS_V : GF_MINB_ROWS) : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
   pdl_launch();
   pdl_wait();
   GF_BWD_DISPATCH(bwd_row)

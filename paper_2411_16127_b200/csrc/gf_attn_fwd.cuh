@@ -68,7 +68,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? (VAR == GF_ADDV ? GF_U_FWD_V : GF_U_FWD) : (PK ? GF_U2_PK : GF_U2);
+  constexpr int U = CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_U_FWD_H : VAR == GF_ADDV ? GF_U_FWD_V : GF_U_FWD)
+                             : (PK ? GF_U2_PK : GF_U2);
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
   const int4 zero4 = make_int4(0, 0, 0, 0);
@@ -92,7 +93,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
   T al[NE];  // GF_ADDV: this lane's slice of a_l (el = <V[u], a_l> per head)
-  if constexpr (VAR == GF_ADDV) {
+  if constexpr (is_addv(VAR)) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
@@ -128,7 +129,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       rk = inv_norm(head_sum(s, a.LPH));
     }
     }
-  } else if constexpr (VAR == GF_ADDV) {  // er = <V[v], a_r> from the row's own V
+  } else if constexpr (is_addv(VAR)) {  // er = <V[v], a_r> from the row's own V
     T vo[NE], ar[NE];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
@@ -186,7 +187,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
-          } else if constexpr (VAR == GF_ADDV) {
+          } else if constexpr (is_addv(VAR)) {
             // el from the gathered V row (after the slot loop)
           } else {
             s[t] = ld_node(Qb + uu * qs);
@@ -215,7 +216,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
             s[t] = a.scale * d;
-          } else if constexpr (VAR == GF_ADDV) {
+          } else if constexpr (is_addv(VAR)) {
             s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
@@ -284,7 +285,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
               ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
-          } else if constexpr (VAR == GF_ADDV) {
+          } else if constexpr (is_addv(VAR)) {
             // el from the gathered V row (after the slot loop)
           } else {
             s[t] = ld_node(Qb + uu * qs);
@@ -313,7 +314,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
             s[t] = a.scale * d;
-          } else if constexpr (VAR == GF_ADDV) {
+          } else if constexpr (is_addv(VAR)) {
             s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
@@ -443,7 +444,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
 // warps), warp rows, and packed rows (degree <= kSmallDegree, EPW rows per
 // warp, one LPE-lane group each); the bucket is warp-uniform.
 template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_FWD : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_MINB_FWD_H : VAR == GF_ADDV ? GF_MINB_FWD_V : GF_MINB_FWD) : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
   pdl_launch();
   pdl_wait();
   constexpr int EPW = 32 / LPE;
@@ -584,6 +585,8 @@ int launch_fast_fwd(const FwdArgs<T>& a, int variant, int mode, int blocks, cuda
     GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_DOT>, blocks, 256, s, a));
   else if (variant == GF_ADDV)
     GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADDV>, blocks, 256, s, a));
+  else if (variant == GF_ADDV_HBM)
+    GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADDV_HBM>, blocks, 256, s, a));
   else
     GF_CHECK_CUDA(launch_k(fwd_fast<T, CB, LPE, CPL, GF_ADD>, blocks, 256, s, a));
   GF_CHECK_LAUNCH("fwd_fast");
@@ -658,6 +661,11 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     set_error("gf_attn_fwd: logits-from-V needs the fast path (callers fall back to el/er tables)");
     return GF_ERR_INVALID;
   }
+  // layer form with the gathered V table far beyond L2 (HBM-bound, C5): the
+  // high-occupancy instantiation (profiles/r2/ab_r2_gat_layer_form.txt)
+  if (variant == GF_ADDV &&
+      static_cast<int64_t>(g.n) * a.F * static_cast<int64_t>(sizeof(T)) > (int64_t(100) << 20))
+    variant = GF_ADDV_HBM;
   if (al) {
     a.LPH = fs.lph;
     const int epw = 32 / fs.lpe;

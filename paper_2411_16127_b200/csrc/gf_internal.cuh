@@ -19,6 +19,11 @@ namespace gfb {
 // 116-125, V = H), so no el table is gathered per edge.  Q / K carry a_l / a_r
 // (H x D, the layout of a V row).  Internal: not a gf_attn_desc.variant value.
 constexpr int GF_ADDV = 2;
+// The same layer form tuned for gathered tables far beyond L2 (HBM-bound, short
+// rows: C5): more resident warps, fewer edges in flight per warp
+// (GF_MINB_FWD_H / GF_U_FWD_H); selected by the forward launcher per graph.
+constexpr int GF_ADDV_HBM = 3;
+__host__ __device__ constexpr bool is_addv(int v) { return v == GF_ADDV || v == GF_ADDV_HBM; }
 
 // ------------------------------------------------------------------ errors --
 void set_error(const std::string& msg);
@@ -143,11 +148,23 @@ struct DevGraph {
 #ifndef GF_U2
 #define GF_U2 1
 #endif
+#ifndef GF_MINB_FWD_V
+#define GF_MINB_FWD_V GF_MINB_FWD  // GAT layer form (GF_ADDV) forward
+#endif
+#ifndef GF_MINB_ROWS_V
+#define GF_MINB_ROWS_V 4  // GAT layer form pass A (C4 1.91 -> 1.83 ms, C5 GAT 3.43 -> 3.06)
+#endif
+#ifndef GF_MINB_FWD_H
+#define GF_MINB_FWD_H 4
+#endif
+#ifndef GF_U_FWD_H
+#define GF_U_FWD_H 2
+#endif
 #ifndef GF_U_FWD_V
 #define GF_U_FWD_V GF_U_FWD  // GAT layer form (GF_ADDV) forward
 #endif
 #ifndef GF_U_ROWS_V
-#define GF_U_ROWS_V GF_U_ROWS  // GAT layer form pass A
+#define GF_U_ROWS_V 2  // GAT layer form pass A
 #endif
 #ifndef GF_U2_PK
 #define GF_U2_PK 1  // packed rows of two-chunk lanes (A/B knob)
