@@ -196,8 +196,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
         if constexpr (MODE >= 2) {
   #pragma unroll
           for (int t = 0; t < U; ++t) {
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
+            axpy_n(acc, s[t], vv[t]);
           }
           continue;
         }
@@ -229,16 +228,14 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           const T mn = smax > m ? smax : m;
           const T corr = m == mn ? T(1) : expd(m - mn);
           l *= corr;
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] *= corr;
+          scale_n(acc, corr);
           m = mn;
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const T p = ok[t] ? expd(s[t] - m) : T(0);
           l += p;
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
+          axpy_n(acc, p, vv[t]);
         }
       }
     };
@@ -294,8 +291,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
         if constexpr (MODE >= 2) {
   #pragma unroll
           for (int t = 0; t < U; ++t) {
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) acc[i] += s[t] * vv[t][i];
+            axpy_n(acc, s[t], vv[t]);
           }
           continue;
         }
@@ -327,16 +323,14 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           const T mn = smax > m ? smax : m;
           const T corr = m == mn ? T(1) : expd(m - mn);
           l *= corr;
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] *= corr;
+          scale_n(acc, corr);
           m = mn;
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const T p = ok[t] ? expd(s[t] - m) : T(0);
           l += p;
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) acc[i] += p * vv[t][i];
+          axpy_n(acc, p, vv[t]);
         }
       }
     }

@@ -13,8 +13,85 @@ constexpr unsigned kFull = 0xffffffffu;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+// Element-pair arithmetic: on sm_100 fp32 pairs map to FFMA2 / FMUL2 (one
+// instruction for two lanes' worth of FMAs) — the fused kernels are partly
+// issue-bound, and the per-edge accumulator updates are their biggest FP
+// share.  Per element the result is the same IEEE fma / mul as the scalar
+// form; fp64 keeps scalar code.
+#ifndef GF_PAIRED_FP
+#define GF_PAIRED_FP 1
+#endif
+template <typename T, int N>
+__device__ __forceinline__ void axpy_n(T (&y)[N], T a, const T (&x)[N]) {
+#if GF_PAIRED_FP
+  if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+    const float2 aa = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const float2 r = __ffma2_rn(aa, make_float2(x[i], x[i + 1]), make_float2(y[i], y[i + 1]));
+      y[i] = r.x;
+      y[i + 1] = r.y;
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] += a * x[i];
+}
+
+// y[OFF + i] += a x[i] for the first N elements at offset OFF of a longer
+// accumulator array (pass B's {dV | dQ} registers).
+template <int OFF, typename T, int N, int M>
+__device__ __forceinline__ void axpy_at(T (&y)[M], T a, const T (&x)[N]) {
+  static_assert(OFF + N <= M, "axpy_at range");
+#if GF_PAIRED_FP
+  if constexpr (sizeof(T) == 4 && N % 2 == 0 && OFF % 2 == 0) {
+    const float2 aa = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const float2 r =
+          __ffma2_rn(aa, make_float2(x[i], x[i + 1]), make_float2(y[OFF + i], y[OFF + i + 1]));
+      y[OFF + i] = r.x;
+      y[OFF + i + 1] = r.y;
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[OFF + i] += a * x[i];
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void scale_n(T (&y)[N], T a) {
+#if GF_PAIRED_FP
+  if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+    const float2 aa = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const float2 r = __fmul2_rn(aa, make_float2(y[i], y[i + 1]));
+      y[i] = r.x;
+      y[i + 1] = r.y;
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] *= a;
+}
+
+// <x, y>: fp32 pairs accumulate even / odd elements in two FFMA2 lanes, then
+// add them (a pairwise order; fp64 and odd N sequential).
 template <typename T, int N>
 __device__ __forceinline__ T dot_n(const T (&x)[N], const T (&y)[N]) {
+#if GF_PAIRED_FP
+  if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+      acc = __ffma2_rn(make_float2(x[i], x[i + 1]), make_float2(y[i], y[i + 1]), acc);
+    return acc.x + acc.y;
+  }
+#endif
   T s = T(0);
 #pragma unroll
   for (int i = 0; i < N; ++i) s += x[i] * y[i];
