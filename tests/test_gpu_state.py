@@ -53,3 +53,36 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=ROOT, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_pdl_and_split_overrides_keep_results(cuda):
+    """Programmatic dependent launch (default) vs GF_PDL=0, and a forced
+    multi-CTA split (GF_SPLIT_LEN=100) vs the default: forward and backward
+    results are bitwise equal for PDL and oracle-equal for the split."""
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+sys.path.insert(0, %r + "/tests")
+from test_gpu_parity import make_graph, make_inputs, run_device
+from paper_2411_16127_b200.fused import AttnSpec
+g = make_graph("hub")
+spec = AttnSpec(variant="dot", heads=8, head_dim=16, scale=0.25)
+Q, K, V, dO = make_inputs(g, "dot", 8, 16, np.float32, 3)
+r = run_device(g, spec, Q, K, V, dO)
+np.savez(sys.argv[1], **r)
+""" % (ROOT, ROOT)
+    outs = {}
+    for name, env_extra in (("pdl", {}), ("nopdl", {"GF_PDL": "0"}), ("split", {"GF_SPLIT_LEN": "100"})):
+        env = dict(os.environ, **env_extra)
+        path = os.path.join(ROOT, "gpurun_out", f"_state_{name}.npz")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                           env=env, cwd=ROOT, timeout=300)
+        assert r.returncode == 0, r.stderr[-3000:]
+        import numpy as np
+
+        outs[name] = dict(np.load(path))
+    for k in ("O", "dQ", "dK", "dV"):
+        assert (outs["pdl"][k] == outs["nopdl"][k]).all(), k
+        a, b = outs["pdl"][k], outs["split"][k]
+        assert float(abs(a - b).max() / max(1.0, float(abs(a).max()))) < 1e-5, k
