@@ -395,6 +395,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
 template <typename T, int CB, int LPE, int CPL, int VAR>
 __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV ? GF_MINB_ROWS_V : GF_MINB_ROWS) : GF_MINB2) bwd_rows_fast(const BwdArgs<T> a) {
   pdl_launch();
+  if (a.pf_len[0] > 0) l2_prefetch_tables(a.pf_ptr, a.pf_len);
   pdl_wait();
   GF_BWD_DISPATCH(bwd_row)
 }
@@ -654,6 +655,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_c
   // one call site for CTA and warp columns (runtime `cta`): two inlined copies
   // push pass B past its 64-register budget
   pdl_launch();
+  if (a.pf_len[0] > 0) l2_prefetch_tables(a.pf_ptr, a.pf_len);
   pdl_wait();
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -928,6 +930,23 @@ int launch_bwd(const DevGraph& g, BwdArgs<T> a, int variant, int passes, cudaStr
   };
   const int rb = (do_a && fast_a) ? buckets(ra, g.n_small_rows, g.n_empty_rows) : 0;
   const int cbk = (do_b && fast_b) ? buckets(ca, g.n_small_cols, g.n_empty_cols) : 0;
+  // small graphs: prefetch each pass's gathered tables into L2 at entry
+  // (pass A: V, Q|el, dO; pass B: dO, K (dot), the records)
+  if (l2_prefetch_enabled() && g.e < kPrefetchMaxEdges) {
+    const int64_t fb = static_cast<int64_t>(g.n) * a.F * static_cast<int64_t>(sizeof(T));
+    const int64_t qb = dot ? fb : is_addv(variant) ? 0 : static_cast<int64_t>(g.n) * a.H * sizeof(T);
+    const int64_t rb = static_cast<int64_t>(g.n) * a.H * 4 * static_cast<int64_t>(sizeof(T));
+    if (2 * fb + qb <= kPrefetchMaxBytes) {
+      ra.pf_ptr[0] = a.V, ra.pf_len[0] = fb;
+      ra.pf_ptr[1] = a.Q, ra.pf_len[1] = qb;
+      ra.pf_ptr[2] = a.dO, ra.pf_len[2] = fb;
+    }
+    if (fb + (dot ? fb : 0) + rb <= kPrefetchMaxBytes) {
+      ca.pf_ptr[0] = a.dO, ca.pf_len[0] = fb;
+      ca.pf_ptr[1] = a.K, ca.pf_len[1] = dot ? fb : 0;
+      ca.pf_ptr[2] = a.stats, ca.pf_len[2] = rb;
+    }
+  }
   // split super rows / columns: slice partials + arrival counters
   const size_t ne = fs.ok ? static_cast<size_t>(fs.cpl) * (fs.cb / sizeof(T)) : 0;
   auto parts = [&](BwdArgs<T>& x, size_t nv) -> int {

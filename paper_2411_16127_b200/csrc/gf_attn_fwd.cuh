@@ -440,6 +440,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
 template <typename T, int CB, int LPE, int CPL, int VAR, int MODE = 0>
 __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_MINB_FWD_H : VAR == GF_ADDV ? GF_MINB_FWD_V : GF_MINB_FWD) : GF_MINB2) fwd_fast(const FwdArgs<T> a) {
   pdl_launch();
+  if (a.pf_len[0] > 0) l2_prefetch_tables(a.pf_ptr, a.pf_len);
   pdl_wait();
   constexpr int EPW = 32 / LPE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -675,6 +676,17 @@ int launch_fwd_mode(const DevGraph& g, const FwdArgs<T>& a0, int variant, int mo
     const int rows_per_block = kWarpsPerBlock * epw;
     const int cta_blocks = a.cta_tab ? a.cta_blocks : a.n_cta;
     const int blocks = cta_blocks + a.wblocks + (a.n - a.pk0 + rows_per_block - 1) / rows_per_block;
+    if (l2_prefetch_enabled() && a.e < kPrefetchMaxEdges && mode <= 1) {
+      // the gathered tables: V, and Q (dot) | el (table-form GAT)
+      const int64_t vb = static_cast<int64_t>(g.n) * a.F * static_cast<int64_t>(sizeof(T));
+      const int64_t qb = variant == GF_DOT ? vb
+                         : is_addv(variant) ? 0
+                                            : static_cast<int64_t>(g.n) * a.H * sizeof(T);
+      if (vb + qb <= kPrefetchMaxBytes) {
+        a.pf_ptr[0] = a.V, a.pf_len[0] = vb;
+        a.pf_ptr[1] = a.Q, a.pf_len[1] = qb;
+      }
+    }
     // split super rows: slice states + arrival counters (stream-ordered scratch)
     if (a.cta_tab && a.parts > 0) {
       const size_t nv = 2 + static_cast<size_t>(fs.cpl) * (fs.cb / sizeof(T));

@@ -55,6 +55,13 @@ cudaMemPool_t scratch_pool(int dev) { return dev >= 0 && dev < 64 ? pools[dev] :
 
 
 namespace gfb {
+bool l2_prefetch_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GF_L2_PREFETCH");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("GF_PDL");

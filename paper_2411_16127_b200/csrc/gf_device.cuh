@@ -8,6 +8,21 @@
 namespace gfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+// Every thread of the grid prefetches its share of up to three node tables
+// into L2 (prefetch.global.L2, one 128 B line per request).  A hint only:
+// it never changes results, so it may run before pdl_wait.
+__device__ __forceinline__ void l2_prefetch_tables(const void* const (&p)[3],
+                                                   const int64_t (&len)[3]) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const char* b = static_cast<const char*>(p[k]);
+    for (int64_t off = tid * 128; off < len[k]; off += nth * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(b + off));
+  }
+}
+
 // PDL (gf_internal.cuh launch_k): wait for the previous grid's completion and
 // memory before touching global memory; let the next grid be scheduled.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

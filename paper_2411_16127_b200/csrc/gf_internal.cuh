@@ -214,6 +214,13 @@ cudaError_t launch_k(Kern k, int blocks, int threads, cudaStream_t s, const Arg&
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, a);
 }
+// Small graphs (E below this) prefetch their gathered node tables into L2 at
+// kernel entry: with L2 cold the passes are bound by dependent DRAM round
+// trips, and L2 hits cut each gather's latency (GF_L2_PREFETCH=0 disables).
+constexpr int64_t kPrefetchMaxEdges = int64_t(4) << 20;
+constexpr int64_t kPrefetchMaxBytes = int64_t(96) << 20;
+bool l2_prefetch_enabled();
+
 // Edges per CTA slice of a split row: no CTA of a pass holds more than ~1/4
 // of one SM's share of the edges (148 SMs), and never fewer than a CTA row.
 // GF_SPLIT_LEN=<edges> overrides (A/B; a huge value disables splitting).
@@ -253,6 +260,10 @@ struct FwdArgs {
   int cta_blocks = 0, parts = 0;
   T* part = nullptr;           // parts x LPE x (2 + NE) slice states
   unsigned* part_cnt = nullptr;  // arrivals per split row (indexed by its first partial)
+  // small graphs: node tables the launch gathers, prefetched into L2 by every
+  // thread's first instructions (see l2_prefetch_tables)
+  const void* pf_ptr[3] = {nullptr, nullptr, nullptr};
+  int64_t pf_len[3] = {0, 0, 0};
 };
 
 template <typename T>
@@ -280,6 +291,8 @@ struct BwdArgs {
   int cta_blocks = 0, parts = 0;
   T* part = nullptr;
   unsigned* part_cnt = nullptr;
+  const void* pf_ptr[3] = {nullptr, nullptr, nullptr};  // L2 prefetch (as FwdArgs)
+  int64_t pf_len[3] = {0, 0, 0};
 };
 
 // Launchers (defined in gf_attn_fwd.cuh / gf_attn_bwd.cuh).
