@@ -787,8 +787,21 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
     # symmetric memory, device barrier); "nccl" = projection, then all-gather.
     pt, exchange = None, None
     if shard is not None:
+        import torch.distributed as dist
+
         exchange = args.dist_backend  # all-gather over the process group
+        cap = 0
         if getattr(args, "exchange", "p2p") == "p2p" and args.dist_backend == "nccl":
+            try:  # every rank must be able to, or none tries (rendezvous is collective)
+                import torch.distributed._symmetric_memory  # noqa: F401
+
+                cap = 1
+            except Exception:
+                cap = 0
+            capt = torch.tensor([cap], dtype=torch.int32, device=dev)
+            dist.all_reduce(capt, op=dist.ReduceOp.MIN)
+            cap = int(capt.item())
+        if cap:
             try:
                 from paper_2411_16127_b200.shard import PeerTables
 
@@ -797,6 +810,7 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
                 pt.selftest()
                 exchange = "p2p: gemm_bcast epilogue into symmetric-memory tables + device barrier"
             except Exception as ex:  # recorded in the JSON line, NCCL path used
+                pt = None
                 exchange = f"nccl (p2p unavailable: {type(ex).__name__}: {str(ex)[:120]})"
     Hf = pt.table("V") if pt is not None else torch.zeros(n, F, device=dev)
     Qb = pt.table("Q") if pt is not None and not gat_layer(layer) else torch.zeros(n, F, device=dev)

@@ -192,6 +192,8 @@ class PeerTables:
         into its block of every copy of the first table, barrier, and every
         block of the local copy must then hold its owner's value.  Raises on a
         mismatch (the caller falls back to the NCCL exchange)."""
+        import torch.distributed as dist
+
         name = next(iter(self.offsets))
         R = self.shard.R
         t = self.table(name)
@@ -201,9 +203,14 @@ class PeerTables:
         self.barrier()
         got = t.view(self.shard.world, R, -1)[:, :, 0].cpu()
         want = torch.arange(1, self.shard.world + 1, dtype=got.dtype)[:, None].expand_as(got)
-        if not torch.equal(got, want):
+        ok = torch.equal(got, want)
+        self.barrier()  # every rank passes every barrier whatever its verdict
+        # all ranks take the same decision (a rank falling back alone would
+        # leave the others waiting in a device barrier)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=t.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
             raise RuntimeError("PeerTables.selftest: peer writes did not land in every copy")
-        self.barrier()
 
     def barrier(self):
         """Device-side barrier on the current stream: every rank's writes
