@@ -358,6 +358,12 @@ int gf_measure_metrics(void (*prep)(void*), void (*fn)(void*), void* user,
  * an L2-resident footprint, the roofline denominator for the gather kernels. */
 int gf_measure_l2_gather(size_t footprint_bytes, int32_t row_bytes, int32_t iters,
                          double* gbs_out, void* stream);
+/* Design probe (profiles/r2/ab_r2_passb_alternatives.txt): mean ms of a
+ * scatter over the CSC edges of a device graph's arrays into table[v][0..7]
+ * (mode 0 red.add.f32, 1 red.add.v4.f32, 2 st.f32, 3 ld.f32, 4 red.add.u64),
+ * `iters` launches after a warm-up. */
+int gf_probe_scatter(int64_t n, const int32_t* csc_ptr, const int32_t* csc_row, float* table,
+                     int32_t mode, int32_t iters, float* ms_out, void* stream);
 
 #ifdef __cplusplus
 }

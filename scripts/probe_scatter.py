@@ -12,9 +12,6 @@ from paper_2411_16127_b200 import fused  # noqa: E402
 from paper_2411_16127_b200._capi import check, lib  # noqa: E402
 
 L = lib()
-L.gf_probe_scatter.restype = C.c_int
-L.gf_probe_scatter.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
-                               C.POINTER(C.c_float), C.c_void_p]
 dev = torch.device("cuda")
 n, src, dst = bench.gen_graph_device("reddit", dev)
 rp, col, cp, cr, _ = fused.from_coo_device(n, src, dst)

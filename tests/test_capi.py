@@ -55,3 +55,20 @@ def test_error_reporting_without_device():
     assert b"invalid descriptor" in lib.gf_last_error()
     rc = lib.gf_graph_create(-1, 0, None, None, None, None, 0, None, C.byref(C.c_void_p()))
     assert rc == 1
+
+
+def test_descriptor_flags_validated_without_device():
+    """GF_FLAG_LOGITS_FROM_V is only valid with the additive variant; unknown
+    flag bits are rejected; the single-step ops take no flags."""
+    import ctypes as C
+
+    lib = _capi.lib()
+    dot_flag = _capi.AttnDesc(0, 0, 0, 8, 8, _capi.GF_FLAG_LOGITS_FROM_V, 1.0, 0.2)
+    rc = lib.gf_attn_fwd(C.c_void_p(1), C.byref(dot_flag), None, None, None, None, None, None,
+                         None)
+    assert rc == 1 and b"flags" in lib.gf_last_error()
+    bad_bits = _capi.AttnDesc(0, 1, 0, 8, 8, 6, 1.0, 0.2)
+    assert lib.gf_attn_bwd(C.c_void_p(1), C.byref(bad_bits), *([None] * 10)) == 1
+    ok_flag = _capi.AttnDesc(0, 1, 0, 8, 8, _capi.GF_FLAG_LOGITS_FROM_V, 1.0, 0.2)
+    assert lib.gf_sddmm(C.c_void_p(1), C.byref(ok_flag), None, None, None, None) == 1
+    assert b"no descriptor flags" in lib.gf_last_error()
