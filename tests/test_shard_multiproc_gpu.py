@@ -30,3 +30,22 @@ def test_sharded_step_across_processes(cuda, world, model):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("SHARD-OK") == world, out[-4000:]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("model", ["gat_layer", "gt"])
+def test_phased_forward_across_processes(cuda, world, model):
+    """The source-phased forward (per-owner broadcasts, one forward per source
+    block, gf_attn_merge_parts) across real ranks == 1 GPU up to the merge's
+    fp32 rounding (2e-5), backward included."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "tests", "mp_shard_worker.py"), "--model", model, "--phased"]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count("SHARD-OK") == world, out[-4000:]
