@@ -858,10 +858,9 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             else:
                 fused.gat_logits(Hf[rows], al, ar, H, D, stream=stream, el=EL[rows], er=ER[rows])
                 q, k, v = EL, ER, Hf
-        else:
-            fused.gemm(Xr, Wq, out=Qb[rows], stream=stream)
-            fused.gemm(Xr, Wk, out=Kb[rows], stream=stream)
-            fused.gemm(Xr, Wv, out=Hf[rows], stream=stream)
+        else:  # X·[W_q | W_k | W_v] as one tcgen05 GEMM, X read once (gf_gemm_split)
+            fused.gemm_split(Xr, torch.cat([Wq, Wk, Wv], 1), [Qb[rows], Kb[rows], Hf[rows]],
+                             stream=stream)
             q, k, v = Qb, Kb, Hf
         if shard is not None and pt is None:  # source rows first; dO (and K) under fwd / pass A
             for w in [all_gather_rows(t, shard, async_op=True)
@@ -917,7 +916,8 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             "sgd_ms": seg(3),
             "step": "projection (+ all-gather when sharded) -> fused attention fwd + recompute "
                     "bwd -> GAT fan-in -> X^T dY (+ all-reduce when sharded) -> SGD update",
-            "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; X^T*dY deterministic split-K)",
+            "projection": "X*W and X^T*dY on tcgen05 (3xTF32, UTCHMMA; GT/AGNN X*[Wq|Wk|Wv] as one "
+                          "split-output GEMM; X^T*dY deterministic split-K)",
             "exchange": exchange,
             "x_width": F}
 

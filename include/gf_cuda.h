@@ -286,6 +286,18 @@ int gf_attn_merge_parts(int32_t dtype, int64_t rows, int32_t heads, int32_t head
  * Replaces models.hpp:116-125's projections + the row all-gather. */
 int gf_gemm_bcast(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
                   void* const* dst, int32_t n_dst, void* stream);
+/* C = A·B (fp32, 3xTF32 tcgen05, TMA epilogue) with column block j (N / n_dst
+ * columns, a multiple of 32) stored to dst[j] (row-major M x N / n_dst): the
+ * GT / AGNN projections X·[W_q | W_k | W_v] as one GEMM writing Q, K, V into
+ * their own tables (models.hpp:116-125).  16 B aligned, K % 4 == 0. */
+int gf_gemm_split(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
+                  void* const* dst, int32_t n_dst, void* stream);
+/* C = A·B (fp32, 3xTF32 tcgen05, TMA epilogue) with column block j (N / n_dst
+ * columns, a multiple of 32) stored to dst[j] (row-major M x N / n_dst): the
+ * GT / AGNN projections X·[W_q | W_k | W_v] as one GEMM writing Q, K, V into
+ * their own tables (models.hpp:116-125).  16 B aligned, K % 4 == 0. */
+int gf_gemm_split(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
+                  void* const* dst, int32_t n_dst, void* stream);
 /* GAT attention logits: el[n,h] = sum_d Hf[n,h,d] a_l[h,d]; er likewise. */
 int gf_gat_logits(int32_t dtype, int64_t n, int32_t H, int32_t D, const void* Hf, const void* a_l,
                   const void* a_r, void* el, void* er, void* stream);

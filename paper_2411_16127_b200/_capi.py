@@ -109,6 +109,10 @@ SIGNATURES = {
                                       C.POINTER(C.c_void_p), _vp, _vp, _vp]),
     "gf_gemm_bcast": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp,
                                 C.POINTER(C.c_void_p), C.c_int32, _vp]),
+    "gf_gemm_split": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp,
+                                C.POINTER(C.c_void_p), C.c_int32, _vp]),
+    "gf_gemm_split": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp,
+                                C.POINTER(C.c_void_p), C.c_int32, _vp]),
     "gf_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp,
                           C.c_int32, _vp]),
     "gf_gat_logits": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,

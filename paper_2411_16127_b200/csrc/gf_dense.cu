@@ -23,7 +23,8 @@ int tc_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, flo
 bool tma_gemm_eligible(int dtype, int trans_a, int64_t M, int64_t N, int64_t K, const void* A,
                        const void* C);
 int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
-             int accumulate, cudaStream_t s, float* const* peer_c = nullptr, int n_peers = 0);
+             int accumulate, cudaStream_t s, float* const* peer_c = nullptr, int n_peers = 0,
+             int split_w = 0);
 bool tc_gemm_tn_eligible(int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                          const void* B);
 int tc_gemm_tn(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
@@ -460,4 +461,33 @@ extern "C" int gf_gemm_bcast(int32_t dtype, int64_t M, int64_t N, int64_t K, con
   return gfb::tma_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
                        static_cast<float*>(dst[0]), 0, static_cast<cudaStream_t>(stream), peers,
                        n_dst - 1);
+}
+
+// C = A·B with column block j (N / n_dst wide) stored to dst[j] (row-major M x
+// N / n_dst): the GT / AGNN projections X·[W_q | W_k | W_v] as ONE tcgen05
+// GEMM (X read once) whose TMA epilogue writes Q, K and V into their own
+// tables (models.hpp:116-125).
+extern "C" int gf_gemm_split(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                             const void* B, void* const* dst, int32_t n_dst, void* stream) {
+  if (!dst || n_dst < 1 || n_dst > 8 || M < 0 || N < 0 || K < 0 || M >= (1LL << 31) ||
+      N >= (1LL << 31) || K >= (1LL << 31) || (n_dst > 0 && N % n_dst)) {
+    gfb::set_error("gf_gemm_split: invalid arguments (1 <= n_dst <= 8, N % n_dst == 0)");
+    return GF_ERR_INVALID;
+  }
+  for (int i = 0; i < n_dst; ++i)
+    if (!dst[i] || (reinterpret_cast<uintptr_t>(dst[i]) & 15u)) {
+      gfb::set_error("gf_gemm_split: destinations must be non-null and 16 B aligned");
+      return GF_ERR_INVALID;
+    }
+  if (M == 0 || N == 0) return GF_OK;
+  const int64_t w = N / n_dst;
+  if (!gfb::tma_gemm_eligible(dtype, 0, M, N, K, A, dst[0]) || w % 32) {
+    gfb::set_error("gf_gemm_split: needs fp32, K % 4 == 0, (N / n_dst) % 32 == 0, 16 B aligned");
+    return GF_ERR_INVALID;
+  }
+  float* rest[8];
+  for (int i = 1; i < n_dst; ++i) rest[i - 1] = static_cast<float*>(dst[i]);
+  return gfb::tma_gemm(M, N, K, static_cast<const float*>(A), static_cast<const float*>(B),
+                       static_cast<float*>(dst[0]), 0, static_cast<cudaStream_t>(stream), rest,
+                       n_dst - 1, static_cast<int>(w));
 }

@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const __grid_constant__ CUtensorMap map_blo,
                     const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ PeerMaps peers, int M, int N, int K, int nt,
-                    int stages, int bres, int tma_out, float* __restrict__ C, int accumulate) {
+                    int stages, int bres, int tma_out, float* __restrict__ C, int accumulate,
+                    int split_w) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024 B-align the stage area (the swizzle pattern assumes it)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -315,9 +316,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           epi_bar();
           if (t == 0) {
-            tma_store_2d(&map_c, n_idx * nt + c0, m * TM, buf, accumulate != 0);
-            for (int p = 0; p < peers.n; ++p)  // same tile into the peers' tables
-              tma_store_2d(&peers.map[p], n_idx * nt + c0, m * TM, buf, accumulate != 0);
+            const int col = n_idx * nt + c0;
+            if (split_w > 0) {  // column block j of C goes to destination j
+              const int j = col / split_w;
+              tma_store_2d(j == 0 ? &map_c : &peers.map[j - 1], col - j * split_w, m * TM, buf,
+                           accumulate != 0);
+            } else {
+              tma_store_2d(&map_c, col, m * TM, buf, accumulate != 0);
+              for (int p = 0; p < peers.n; ++p)  // same tile into the peers' tables
+                tma_store_2d(&peers.map[p], col, m * TM, buf, accumulate != 0);
+            }
             bulk_commit();
           }
         }
@@ -412,7 +420,7 @@ int env_int(const char* name, int dflt) {
 }
 
 int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C,
-             int accumulate, cudaStream_t s, float* const* peer_c, int n_peers) {
+             int accumulate, cudaStream_t s, float* const* peer_c, int n_peers, int split_w) {
   if (n_peers < 0 || n_peers > kMaxPeers) {
     set_error("gf_gemm_bcast: at most 8 destinations");
     return GF_ERR_INVALID;
@@ -421,6 +429,10 @@ int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, fl
   int nt = pick_nt(N);
   const int nt_env = env_int("GF_TMA_NT", 0);
   if (nt_env >= 16 && nt_env <= 128 && nt_env % 16 == 0 && N % nt_env == 0) nt = nt_env;
+  if (split_w > 0 && (split_w % 32 || N != static_cast<int64_t>(split_w) * (n_peers + 1) || nt % 32)) {
+    set_error("gf_gemm_split: every destination must be a multiple of 32 columns wide");
+    return GF_ERR_INVALID;
+  }
   float* bsplit = nullptr;
   GF_CHECK_CUDA(scratch_alloc(&bsplit, sizeof(float) * 2 * N * K, s));
   float *braw = bsplit, *blo = bsplit + N * K;
@@ -437,9 +449,10 @@ int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, fl
     return GF_ERR_INVALID;
   }
   bool peer_ok = true;
-  for (int p = 0; p < n_peers; ++p) peer_ok = peer_ok && make_map(&pm.map[p], peer_c[p], M, N, TM);
+  const int64_t cw = split_w > 0 ? split_w : N;  // columns of each destination
+  for (int p = 0; p < n_peers; ++p) peer_ok = peer_ok && make_map(&pm.map[p], peer_c[p], M, cw, TM);
   if (!peer_ok || !make_map(&ma, A, M, K, TM) || !make_map(&mbr, braw, N, K, nt) ||
-      !make_map(&mbl, blo, N, K, nt) || (tma_out && !make_map(&mc, C, M, N, TM))) {
+      !make_map(&mbl, blo, N, K, nt) || (tma_out && !make_map(&mc, C, M, cw, TM))) {
     cudaFreeAsync(bsplit, s);
     set_error("gf_gemm: cuTensorMapEncodeTiled failed");
     return GF_ERR_CUDA;
@@ -467,7 +480,7 @@ int tma_gemm(int64_t M, int64_t N, int64_t K, const float* A, const float* B, fl
   tma_gemm_kernel<<<grid, NUM_THREADS, smem, s>>>(ma, mbr, mbl, mc, pm, static_cast<int>(M),
                                                   static_cast<int>(N), static_cast<int>(K), nt,
                                                   stages, bres ? 1 : 0, tma_out ? 1 : 0, C,
-                                                  accumulate);
+                                                  accumulate, split_w);
   GF_CHECK_LAUNCH("tma_gemm_kernel");
   cudaFreeAsync(bsplit, s);
   return GF_OK;

@@ -294,6 +294,38 @@ def gemm_bcast(A, B, outs, stream=None):
     return outs[0]
 
 
+def gemm_split(A, B, outs, stream=None):
+    """C = A @ B with column block j of C written to outs[j] (gf_gemm_split):
+    X @ [W_q | W_k | W_v] -> Q, K, V in one tcgen05 GEMM.  fp32, each block
+    a multiple of 32 columns."""
+    M, K = A.shape
+    N = B.shape[1]
+    w = N // max(1, len(outs))
+    for o in outs:
+        if tuple(o.shape) != (M, w) or not o.is_contiguous():
+            raise ValueError("gemm_split: every destination must be a contiguous M x N/len(outs) view")
+    arr = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    check(lib().gf_gemm_split(DTYPES[A.dtype], M, N, K, _p(A), _p(B), arr, len(outs),
+                              _stream(stream)), "gf_gemm_split")
+    return outs
+
+
+def gemm_split(A, B, outs, stream=None):
+    """C = A @ B with column block j of C written to outs[j] (gf_gemm_split):
+    X @ [W_q | W_k | W_v] -> Q, K, V in one tcgen05 GEMM.  fp32, each block
+    a multiple of 32 columns."""
+    M, K = A.shape
+    N = B.shape[1]
+    w = N // max(1, len(outs))
+    for o in outs:
+        if tuple(o.shape) != (M, w) or not o.is_contiguous():
+            raise ValueError("gemm_split: every destination must be a contiguous M x N/len(outs) view")
+    arr = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    check(lib().gf_gemm_split(DTYPES[A.dtype], M, N, K, _p(A), _p(B), arr, len(outs),
+                              _stream(stream)), "gf_gemm_split")
+    return outs
+
+
 def gat_logits(Hf, a_l, a_r, heads, head_dim, stream=None, el=None, er=None):
     n = Hf.shape[0]
     el = torch.empty(n, heads, dtype=Hf.dtype, device=Hf.device) if el is None else el

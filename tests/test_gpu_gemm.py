@@ -148,3 +148,23 @@ def test_gemm_bcast_errors(cuda):
     with pytest.raises(Exception, match="gemm_bcast"):
         fused.gemm_bcast(A, torch.rand(32, 64, device="cuda"),
                          [torch.empty(64, 64, device="cuda")] * 9)
+
+
+@pytest.mark.parametrize("M,F,K", [(1000, 128, 128), (4096, 64, 64), (333, 256, 32)])
+def test_gemm_split_matches_three_gemms(cuda, M, F, K):
+    """X·[W_q | W_k | W_v] as one split-output GEMM == three separate GEMMs,
+    bitwise (same 128-column tiles, same K order)."""
+    import torch
+
+    from paper_2411_16127_b200 import fused
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + F)
+    X = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    Ws = [torch.rand(K, F, device="cuda", generator=g) * 2 - 1 for _ in range(3)]
+    refs = [fused.gemm(X, w) for w in Ws]
+    outs = [torch.empty(M, F, device="cuda") for _ in range(3)]
+    fused.gemm_split(X, torch.cat(Ws, 1), outs)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, refs):
+        assert torch.equal(a, b)
