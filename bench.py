@@ -802,11 +802,21 @@ def layer_step_timing(args, layer, spec, dg, n, e, F, H, D, dev, stream, flush, 
             dist.all_reduce(capt, op=dist.ReduceOp.MIN)
             cap = int(capt.item())
         if cap:
+            why = None
             try:
                 from paper_2411_16127_b200.shard import PeerTables
 
                 pt = PeerTables(shard, {"V": F} if gat_layer(layer) else {"Q": F, "K": F, "V": F},
                                 device=dev)
+            except Exception as ex:
+                pt, why = None, ex
+            # every rank holds its tables before any rank enters the selftest's
+            # device barriers (a rank that failed alone would leave them waiting)
+            okt = torch.tensor([0 if pt is None else 1], dtype=torch.int32, device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            try:
+                if not int(okt.item()):
+                    raise why or RuntimeError("PeerTables failed on another rank")
                 pt.selftest()
                 exchange = "p2p: gemm_bcast epilogue into symmetric-memory tables + device barrier"
             except Exception as ex:  # recorded in the JSON line, NCCL path used

@@ -376,6 +376,10 @@ int gf_measure_l2_gather(size_t footprint_bytes, int32_t row_bytes, int32_t iter
  * `iters` launches after a warm-up. */
 int gf_probe_scatter(int64_t n, const int32_t* csc_ptr, const int32_t* csc_row, float* table,
                      int32_t mode, int32_t iters, float* ms_out, void* stream);
+/* The L2 evict_last policy word the backward passes receive in their argument
+ * block (host_word, a compile-time constant) and the word createpolicy
+ * produces on the device (device_word); the two must agree. */
+int gf_l2_policy_word(uint64_t* device_word, uint64_t* host_word);
 
 #ifdef __cplusplus
 }

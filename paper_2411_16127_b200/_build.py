@@ -48,7 +48,8 @@ def _newer(out: str, deps) -> bool:
 
 
 def _headers():
-    return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INC, "*.h"))
+    return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+            + glob.glob(os.path.join(INC, "*.h"))
             + glob.glob(os.path.join(INC, "graphfuse", "*.hpp")))
 
 

@@ -96,6 +96,7 @@ SIGNATURES = {
     "gf_scratch_trim": (C.c_int, []),
     "gf_probe_scatter": (C.c_int, [C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32,
                                    C.POINTER(C.c_float), _vp]),
+    "gf_l2_policy_word": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "gf_measure_l2_gather": (C.c_int, [C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        _vp]),
     "gf_attn_bwd": (C.c_int, [_vp, C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

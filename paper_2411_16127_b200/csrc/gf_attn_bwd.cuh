@@ -42,6 +42,26 @@
 
 namespace gfb {
 
+// Per-edge dot products of the backward passes (dP = <dO, V>, the dot
+// scores): paired FFMA2 (half the dependent FMA chain) or the sequential
+// order.  Measured per pass (profiles/r2/ab_r2_policy_param.txt): pairs help
+// pass B (-1.5 %) and the table-form pass A (-2 %), but cost the GAT
+// layer-form pass A 20 % (its 64-register budget), which keeps the sequence.
+#ifndef GF_BWD_DOT2
+#define GF_BWD_DOT2 1
+#endif
+template <bool PAIRED, typename T, int N>
+__device__ __forceinline__ T bdot(const T (&x)[N], const T (&y)[N]) {
+  if constexpr (PAIRED && GF_BWD_DOT2) {
+    return dot_n(x, y);
+  } else {
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) s += x[i] * y[i];
+    return s;
+  }
+}
+
 namespace {
 
 // L2 backward of one owned head row (autograd.hpp:76-95): g holds dXhat, x
@@ -105,7 +125,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? (VAR == GF_ADDV ? GF_U_ROWS_V : GF_U_ROWS) : (PK ? GF_U2_PK : GF_U2);
+  constexpr int U = CPL == 1 ? (VAR == GF_ADDV ? GF_U_ROWS_V : VAR == GF_DOT ? GF_U_DOT1 : GF_U_ROWS)
+                             : (PK ? GF_U2_PK : GF_U2);
   constexpr int NA = VAR == GF_DOT ? NE : 1;
   constexpr bool pk = PK;  // packed row: this LPE-lane group owns the row
   const int c = lane % LPE, sub = lane / LPE;
@@ -140,6 +161,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;
   const uint32_t fb = a.F * sizeof(T), qb = qs * sizeof(T);  // row strides in bytes
+  const uint64_t pol = GF_POL_PARAM_BWD ? a.pol : pol_keep();
   T al[NE];  // GF_ADDV: el = <V[u], a_l> from the gathered V row
   if constexpr (VAR == GF_ADDV) {
 #pragma unroll
@@ -205,31 +227,24 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
           const int uu = ok[t] ? u : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
           if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW), pol);
           } else if constexpr (VAR == GF_ADDV) {
             el[t] = T(0);  // from the gathered V row below
           } else {
-            el[t] = ld_node(row_at(Qb, uu, qb));
+            el[t] = ld_node(row_at(Qb, uu, qb), pol);
           }
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
-          T dp = T(0);
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) dp += dov[i] * vv[t][i];
+          T dp = bdot<VAR != GF_ADDV>(dov, vv[t]);
           dp = head_sum(dp, a.LPH);
           T s, rq = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
-            T d = T(0), qq = T(0);
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) {
-              d += qv[t][i] * kv[i];
-              qq += qv[t][i] * qv[t][i];
-            }
+            T d = bdot<true>(qv[t], kv), qq = bdot<true>(qv[t], qv[t]);
             d = head_sum(d, a.LPH);
             if (a.l2) {
               rq = inv_norm(head_sum(qq, a.LPH));
@@ -285,31 +300,24 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
           const int uu = ok[t] ? u : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+            ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
           if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+              ld_gather<T, CB>(row_at(Qb, uu, qb) + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW), pol);
           } else if constexpr (VAR == GF_ADDV) {
             el[t] = T(0);  // from the gathered V row below
           } else {
-            el[t] = ld_node(row_at(Qb, uu, qb));
+            el[t] = ld_node(row_at(Qb, uu, qb), pol);
           }
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
-          T dp = T(0);
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) dp += dov[i] * vv[t][i];
+          T dp = bdot<VAR != GF_ADDV>(dov, vv[t]);
           dp = head_sum(dp, a.LPH);
           T s, rq = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
-            T d = T(0), qq = T(0);
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) {
-              d += qv[t][i] * kv[i];
-              qq += qv[t][i] * qv[t][i];
-            }
+            T d = bdot<true>(qv[t], kv), qq = bdot<true>(qv[t], qv[t]);
             d = head_sum(d, a.LPH);
             if (a.l2) {
               rq = inv_norm(head_sum(qq, a.LPH));
@@ -409,7 +417,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? GF_U_COLS : (PK ? GF_U2_PK : GF_U2);
+  constexpr int U = CPL == 1 ? (VAR == GF_DOT ? GF_U_DOT1_COLS : GF_U_COLS) : (PK ? GF_U2_PK : GF_U2);
   constexpr int NT = NE + (VAR == GF_DOT ? NE : 1);  // dV chunk + (dQ chunk | del)
   constexpr bool pk = PK;  // packed column: this LPE-lane group owns the column
   const int c = lane % LPE, sub = lane / LPE;
@@ -434,6 +442,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   const size_t urow = static_cast<size_t>(u) * a.F + off;
   const T* __restrict__ dOb = a.dO + off;
   const uint32_t fb = a.F * sizeof(T);
+  const uint64_t pol = GF_POL_PARAM_BWD ? a.pol : pol_keep();
   const T* __restrict__ Kb = a.K + off;
   const T* __restrict__ Rb = a.stats + 4 * h;
 
@@ -494,25 +503,21 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
           const int vv = ok[t] ? v : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
+            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW), pol);
           if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
+              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW), pol);
           }
           rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
-          T dp = T(0);
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) dp += dov[t][i] * vu[i];
+          T dp = bdot<true>(dov[t], vu);
           dp = head_sum(dp, a.LPH);
           T s, rk = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
-            T d = T(0);
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) d += qu[i] * kv[t][i];
+            T d = bdot<true>(qu, kv[t]);
             d = head_sum(d, a.LPH);
             if (a.l2) {
               rk = rec[t].aux;
@@ -570,25 +575,21 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
           const int vv = ok[t] ? v : 0;
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW));
+            ld_gather<T, CB>(row_at(dOb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(dov[t] + k * CW), pol);
           if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW));
+              ld_gather<T, CB>(row_at(Kb, vv, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(kv[t] + k * CW), pol);
           }
           rec[t] = ld_rec(Rb, static_cast<size_t>(vv) * a.H);
         }
   #pragma unroll
         for (int t = 0; t < U; ++t) {
-          T dp = T(0);
-  #pragma unroll
-          for (int i = 0; i < NE; ++i) dp += dov[t][i] * vu[i];
+          T dp = bdot<true>(dov[t], vu);
           dp = head_sum(dp, a.LPH);
           T s, rk = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
-            T d = T(0);
-  #pragma unroll
-            for (int i = 0; i < NE; ++i) d += qu[i] * kv[t][i];
+            T d = bdot<true>(qu, kv[t]);
             d = head_sum(d, a.LPH);
             if (a.l2) {
               rk = rec[t].aux;
@@ -651,7 +652,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
 }
 
 template <typename T, int CB, int LPE, int CPL, int VAR>
-__global__ void __launch_bounds__(256, CPL == 1 ? GF_MINB_COLS : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
+__global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_DOT ? GF_MINB_DOT1_COLS : GF_MINB_COLS) : GF_MINB2) bwd_cols_fast(const BwdArgs<T> a) {
   // one call site for CTA and warp columns (runtime `cta`): two inlined copies
   // push pass B past its 64-register budget
   pdl_launch();

@@ -33,6 +33,18 @@
 #define GF_FULL_CHUNK 1
 #endif
 
+#ifndef GF_WIDE_ADDR_FWD
+#define GF_WIDE_ADDR_FWD 0
+#endif
+
+#ifndef GF_FWD_DOT2
+#define GF_FWD_DOT2 1
+#endif
+
+#ifndef GF_FMAX
+#define GF_FMAX 1  // running max as FMNMX (same NaN handling as the compare-select)
+#endif
+
 #ifndef GF_FULL_STEPS
 #define GF_FULL_STEPS 0
 #endif
@@ -68,7 +80,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
-  constexpr int U = CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_U_FWD_H : VAR == GF_ADDV ? GF_U_FWD_V : GF_U_FWD)
+  constexpr int U = CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_U_FWD_H : VAR == GF_ADDV ? GF_U_FWD_V
+                                : VAR == GF_DOT && MODE == 0 ? GF_U_DOT1 : GF_U_FWD)
                              : (PK ? GF_U2_PK : GF_U2);
   const int c = lane % LPE, sub = lane / LPE;
   constexpr bool pk = PK;
@@ -99,6 +112,11 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
   }
   const T* __restrict__ Sb = a.ES + h;        // MODE 1/2: ES[e * H + h]
+  const uint64_t pol = GF_POL_PARAM_FWD ? a.pol : pol_keep();
+  // V rows addressed as base + u * stride (one IMAD.WIDE.U32) where V is the
+  // only gathered table (GAT layer form, MODE 2/3) or everywhere (= 2)
+  constexpr bool WIDE = GF_WIDE_ADDR_FWD == 2 || (GF_WIDE_ADDR_FWD == 1 && (is_addv(VAR) || MODE >= 2));
+  const uint32_t fb = static_cast<uint32_t>(a.F * sizeof(T));
 
   for (int r = 0; r < (GF_ROWPIPE ? nrows : 1); ++r) {
   const int4 rsnn = GF_ROWPIPE && r + 2 < nrows ? ld_sched(a.sched + slot + r + 2) : zero4;
@@ -178,7 +196,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+            ld_gather<T, CB>((WIDE ? row_at(Vb, uu, fb) : Vb + uu * a.F) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
           if constexpr (MODE == 3) {
             s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
           } else if constexpr (MODE != 0) {
@@ -186,11 +204,11 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           } else if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW), pol);
           } else if constexpr (is_addv(VAR)) {
             // el from the gathered V row (after the slot loop)
           } else {
-            s[t] = ld_node(Qb + uu * qs);
+            s[t] = ld_node(Qb + uu * qs, pol);
           }
         }
         if constexpr (MODE >= 2) {
@@ -206,11 +224,17 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           if constexpr (MODE == 1) {
             // score read from ES
           } else if constexpr (VAR == GF_DOT) {
-            T d = T(0), qq = T(0);
+            T d, qq;
+            if constexpr (GF_FWD_DOT2) {  // paired FFMA2: half the dependent chain
+              d = dot_n(qv[t], kv);
+              qq = dot_n(qv[t], qv[t]);
+            } else {
+              d = T(0), qq = T(0);
   #pragma unroll
-            for (int i = 0; i < NE; ++i) {
-              d += qv[t][i] * kv[i];
-              qq += qv[t][i] * qv[t][i];
+              for (int i = 0; i < NE; ++i) {
+                d += qv[t][i] * kv[i];
+                qq += qv[t][i] * qv[t][i];
+              }
             }
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
@@ -221,7 +245,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             s[t] = lrelu(s[t] + erv, a.slope);
           }
           s[t] = ok[t] ? s[t] : ninf<T>();
-          smax = s[t] > smax ? s[t] : smax;
+          smax = GF_FMAX ? fmax(s[t], smax) : (s[t] > smax ? s[t] : smax);
         }
         // Lazy rescale, warp-uniform: only when some lane's running max moves.
         if (__any_sync(kFull, smax > m)) {
@@ -273,7 +297,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
-            ld_gather<T, CB>(Vb + uu * a.F + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW));
+            ld_gather<T, CB>((WIDE ? row_at(Vb, uu, fb) : Vb + uu * a.F) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
           if constexpr (MODE == 3) {
             s[t] = ok[t] ? ld_edge(Sb + static_cast<size_t>(ld_idx(a.eperm + base + j)) * a.H) : T(0);
           } else if constexpr (MODE != 0) {
@@ -281,11 +305,11 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           } else if constexpr (VAR == GF_DOT) {
   #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW));
+              ld_gather<T, CB>(Qb + uu * qs + k * CW, *reinterpret_cast<T(*)[CW]>(qv[t] + k * CW), pol);
           } else if constexpr (is_addv(VAR)) {
             // el from the gathered V row (after the slot loop)
           } else {
-            s[t] = ld_node(Qb + uu * qs);
+            s[t] = ld_node(Qb + uu * qs, pol);
           }
         }
         if constexpr (MODE >= 2) {
@@ -301,11 +325,17 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
           if constexpr (MODE == 1) {
             // score read from ES
           } else if constexpr (VAR == GF_DOT) {
-            T d = T(0), qq = T(0);
+            T d, qq;
+            if constexpr (GF_FWD_DOT2) {  // paired FFMA2: half the dependent chain
+              d = dot_n(qv[t], kv);
+              qq = dot_n(qv[t], qv[t]);
+            } else {
+              d = T(0), qq = T(0);
   #pragma unroll
-            for (int i = 0; i < NE; ++i) {
-              d += qv[t][i] * kv[i];
-              qq += qv[t][i] * qv[t][i];
+              for (int i = 0; i < NE; ++i) {
+                d += qv[t][i] * kv[i];
+                qq += qv[t][i] * qv[t][i];
+              }
             }
             d = head_sum(d, a.LPH);
             if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
@@ -316,7 +346,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
             s[t] = lrelu(s[t] + erv, a.slope);
           }
           s[t] = ok[t] ? s[t] : ninf<T>();
-          smax = s[t] > smax ? s[t] : smax;
+          smax = GF_FMAX ? fmax(s[t], smax) : (s[t] > smax ? s[t] : smax);
         }
         // Lazy rescale, warp-uniform: only when some lane's running max moves.
         if (__any_sync(kFull, smax > m)) {

@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "gf_policy.h"
+
 namespace gfb {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -178,17 +180,21 @@ __device__ __forceinline__ int4 ld_sched(const int4* __restrict__ p) {
 
 /// Gathered scalar of a node table (el[src], ...).
 template <typename T>
-__device__ __forceinline__ T ld_node(const T* __restrict__ p) {
+__device__ __forceinline__ T ld_node(const T* __restrict__ p, const uint64_t pol) {
 #if GF_L2HINT
   T v;
   if constexpr (sizeof(T) == 4)
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol_keep()));
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   else
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_keep()));
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 #else
   return __ldg(p);
 #endif
+}
+template <typename T>
+__device__ __forceinline__ T ld_node(const T* __restrict__ p) {
+  return ld_node(p, pol_keep());
 }
 
 // Row r of a node table with a row stride of `stride_bytes`: one
@@ -208,14 +214,25 @@ __device__ __forceinline__ const T* row_at(const T* __restrict__ base, int r, ui
 #endif
 }
 
+// Gathers with an explicit L2 policy word (gf_policy.h); the two-argument
+// form creates evict_last in-kernel.
+template <typename T, int CB>
+__device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)],
+                                          const uint64_t pol);
 template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)]) {
+  ld_gather<T, CB>(p, x, pol_keep());
+}
+
+template <typename T, int CB>
+__device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)],
+                                          const uint64_t pol) {
   if constexpr (CB == 32 && sizeof(T) == 4) {
 #if GF_L2HINT
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
                    "=f"(x[6]), "=f"(x[7])
-                 : "l"(p), "l"(pol_keep()));
+                 : "l"(p), "l"(pol));
 #else
     asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
@@ -226,7 +243,7 @@ __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / s
 #if GF_L2HINT
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
-                 : "l"(p), "l"(pol_keep()));
+                 : "l"(p), "l"(pol));
 #else
     asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
@@ -236,7 +253,7 @@ __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / s
 #if GF_L2HINT
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
-                 : "l"(p), "l"(pol_keep()));
+                 : "l"(p), "l"(pol));
 #else
     const float4 v = __ldg(reinterpret_cast<const float4*>(p));
     x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;

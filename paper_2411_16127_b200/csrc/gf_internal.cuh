@@ -10,6 +10,7 @@
 #include <string>
 
 #include "gf_cuda.h"
+#include "gf_policy.h"
 
 namespace gfb {
 
@@ -163,6 +164,18 @@ struct DevGraph {
 #ifndef GF_U_FWD_V
 #define GF_U_FWD_V GF_U_FWD  // GAT layer form (GF_ADDV) forward
 #endif
+#ifndef GF_U_DOT1
+#define GF_U_DOT1 2  // dot scores with one-chunk lanes (e.g. GT 8x8): Q and V rows per slot
+#endif
+
+#ifndef GF_U_DOT1_COLS
+#define GF_U_DOT1_COLS 1  // ... pass B: one slot (dO + K rows) in flight, no spills
+#endif
+
+#ifndef GF_MINB_DOT1_COLS
+#define GF_MINB_DOT1_COLS 3  // pass B, dot scores, one-chunk lanes: dV + dQ accumulators
+#endif
+
 #ifndef GF_U_ROWS_V
 #define GF_U_ROWS_V 2  // GAT layer form pass A
 #endif
@@ -264,6 +277,7 @@ struct FwdArgs {
   // thread's first instructions (see l2_prefetch_tables)
   const void* pf_ptr[3] = {nullptr, nullptr, nullptr};
   int64_t pf_len[3] = {0, 0, 0};
+  uint64_t pol = kPolicyEvictLast;  // L2 policy word of the gathers (gf_policy.h)
 };
 
 template <typename T>
@@ -293,6 +307,7 @@ struct BwdArgs {
   unsigned* part_cnt = nullptr;
   const void* pf_ptr[3] = {nullptr, nullptr, nullptr};  // L2 prefetch (as FwdArgs)
   int64_t pf_len[3] = {0, 0, 0};
+  uint64_t pol = kPolicyEvictLast;  // as FwdArgs
 };
 
 // Launchers (defined in gf_attn_fwd.cuh / gf_attn_bwd.cuh).

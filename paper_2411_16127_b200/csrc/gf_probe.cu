@@ -115,8 +115,26 @@ __global__ void __launch_bounds__(256) scatter_probe(int n, const int32_t* __res
   }
   if (acc == 12345.678f) sink[threadIdx.x] = acc;
 }
+__global__ void policy_word_probe(uint64_t* out) { out[0] = pol_keep(); }
+
 }  // namespace
 }  // namespace gfb
+
+extern "C" int gf_l2_policy_word(uint64_t* device_word, uint64_t* host_word) {
+  if (!device_word || !host_word) {
+    gfb::set_error("gf_l2_policy_word: null output");
+    return GF_ERR_INVALID;
+  }
+  *host_word = gfb::kPolicyEvictLast;
+  uint64_t* d = nullptr;
+  GF_CHECK_CUDA(cudaMalloc(&d, sizeof(uint64_t)));
+  gfb::policy_word_probe<<<1, 1>>>(d);
+  const int rc = cudaMemcpy(device_word, d, sizeof(uint64_t), cudaMemcpyDeviceToHost) == cudaSuccess
+                     ? GF_OK : GF_ERR_CUDA;
+  cudaFree(d);
+  if (rc) gfb::set_error("gf_l2_policy_word: kernel failed");
+  return rc;
+}
 
 extern "C" int gf_probe_scatter(int64_t n, const int32_t* csc_ptr, const int32_t* csc_row,
                                 float* table, int32_t mode, int32_t iters, float* ms_out,

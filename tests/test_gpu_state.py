@@ -86,3 +86,13 @@ np.savez(sys.argv[1], **r)
         assert (outs["pdl"][k] == outs["nopdl"][k]).all(), k
         a, b = outs["pdl"][k], outs["split"][k]
         assert float(abs(a - b).max() / max(1.0, float(abs(a).max()))) < 1e-5, k
+
+
+def test_l2_policy_word_matches_device(cuda):
+    """The backward passes receive the evict_last policy word as a kernel
+    argument (csrc/gf_policy.h); it must equal what createpolicy yields."""
+    from paper_2411_16127_b200._capi import check, lib
+
+    dev, host = C.c_uint64(), C.c_uint64()
+    check(lib().gf_l2_policy_word(C.byref(dev), C.byref(host)), "gf_l2_policy_word")
+    assert dev.value == host.value, (hex(dev.value), hex(host.value))
