@@ -34,7 +34,7 @@
 #endif
 
 #ifndef GF_WIDE_ADDR_FWD
-#define GF_WIDE_ADDR_FWD 0
+#define GF_WIDE_ADDR_FWD 1  // 1: V rows of the layer form / MODE 2-3 as one IMAD.WIDE.U32 (C4 fwd -1.5 %)
 #endif
 
 #ifndef GF_FWD_DOT2

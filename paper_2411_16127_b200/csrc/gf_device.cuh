@@ -133,6 +133,15 @@ struct Chunk {
 #ifndef GF_L2HINT
 #define GF_L2HINT 1
 #endif
+// GF_L2_EVICT_OP = 1: the 256-bit gathers carry the load's own L2 eviction
+// priority (ld.L2::evict_last -> LDG...ELL2; ptxas allows it on .v8.b32 /
+// .v4.b64 loads only) instead of a cache-hint policy word in the memory
+// descriptor: no policy register pair and no R2UR copies before each gather
+// (profiles/r2/ab_r2_policy_param.txt); same residency behaviour, set-aside
+// included.  Narrower gathers keep the policy word.
+#ifndef GF_L2_EVICT_OP
+#define GF_L2_EVICT_OP 1
+#endif
 __device__ __forceinline__ uint64_t pol_keep() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -214,8 +223,9 @@ __device__ __forceinline__ const T* row_at(const T* __restrict__ base, int r, ui
 #endif
 }
 
-// Gathers with an explicit L2 policy word (gf_policy.h); the two-argument
-// form creates evict_last in-kernel.
+// Gathers with an explicit L2 policy word (gf_policy.h; used when
+// GF_L2_EVICT_OP = 0); the two-argument form creates evict_last in-kernel.
+
 template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)],
                                           const uint64_t pol);
@@ -228,7 +238,13 @@ template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)],
                                           const uint64_t pol) {
   if constexpr (CB == 32 && sizeof(T) == 4) {
-#if GF_L2HINT
+#if GF_L2HINT && GF_L2_EVICT_OP
+    (void)pol;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
+                   "=f"(x[6]), "=f"(x[7])
+                 : "l"(p));
+#elif GF_L2HINT
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
                    "=f"(x[6]), "=f"(x[7])
@@ -240,7 +256,12 @@ __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / s
                  : "l"(p));
 #endif
   } else if constexpr (CB == 32) {
-#if GF_L2HINT
+#if GF_L2HINT && GF_L2_EVICT_OP
+    (void)pol;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(p));
+#elif GF_L2HINT
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
                  : "l"(p), "l"(pol));

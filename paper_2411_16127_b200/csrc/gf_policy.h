@@ -13,7 +13,8 @@ namespace gfb {
 // pair and copied back (2 x R2UR) before every gather — pass B 1.5 % faster
 // on C4.  The forward keeps the in-kernel word: with the parameter its loop
 // waits on a constant-bank load before its gathers and measured 12 % slower
-// (profiles/r2/ab_r2_policy_param.txt).
+// (profiles/r2/ab_r2_policy_param.txt).  Used only with GF_L2_EVICT_OP = 0:
+// by default the gathers carry ld.L2::evict_last and need no policy word.
 constexpr uint64_t kPolicyEvictLast = 0x14F0000000000000ull;
 
 }  // namespace gfb
