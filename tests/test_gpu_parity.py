@@ -127,6 +127,8 @@ CONFIGS = [
     ("dot", True, 2, 5, np.float32),     # generic
     ("add", False, 3, 5, np.float64),    # generic, odd heads
     ("add", False, 4, 2, np.float32),    # generic (D % 4 != 0)
+    ("dot", False, 8, 8, np.float32),    # GT 8x8: one-chunk dot lanes, LPE=8 (U = 2 / pass B U = 1)
+    ("dot", True, 16, 8, np.float32),    # one-chunk dot lanes, LPE=16
 ]
 
 
@@ -503,3 +505,26 @@ def test_gat_layer_form(cuda, graph, dt, path):
                            ("dV", dV, dV_ref)):
         err = rel_err(got.cpu().numpy(), ref)
         assert err <= tol, (name, err)
+
+
+# Seeded sweep over lane geometries x graph shapes x CTA thresholds (the
+# fixed CONFIGS above pin each geometry once; this crosses them with hubs,
+# power-law rows and split super rows).
+_rng = np.random.default_rng(2026)
+SWEEP = []
+for _i in range(16):
+    _var = ["add", "dot"][_rng.integers(0, 2)]
+    _H = int(_rng.choice([1, 2, 4, 8, 16]))
+    _D = int(_rng.choice([4, 8, 16, 32, 64]))
+    while _H * _D > 512:
+        _D //= 2
+    _l2 = bool(_var == "dot" and _rng.integers(0, 2))
+    SWEEP.append((_var, _l2, _H, _D, ["hub", "powerlaw", "random"][_rng.integers(0, 3)],
+                  int(_rng.choice([0, 16, 64, 4096])), int(_rng.integers(1, 1000))))
+
+
+@pytest.mark.parametrize("case", SWEEP, ids=lambda c: f"{c[0]}{'-l2' if c[1] else ''}-{c[2]}x{c[3]}-{c[4]}-t{c[5]}")
+def test_seeded_shape_sweep(cuda, case):
+    variant, l2, H, D, graph, thr, seed = case
+    check_against_oracle(make_graph(graph, seed % 7), variant, l2, H, D, np.float32, seed=seed,
+                         cta_threshold=thr)
