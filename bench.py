@@ -1493,7 +1493,8 @@ def run_ours(args, cfg, rank, world, full=True):
                                  "frac": achieved / peak,
                                  "step_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},
                 "layer": layer_out,
-                "parallelism": (f"row-sharded x{world} (NCCL)" if sharded else "1 GPU")}
+                "parallelism": (f"row-sharded x{world} ({(args.dist_backend or 'nccl').upper()})"
+                                if sharded else "1 GPU")}
     l2_peak, l2_rb = measured_l2_gather(F * 4)
     a_ps, b_ps, g32, g128 = l2_request_costs()
     req_model = {k: l2_request_model_ms(k, layer, H, D, e_of[k], a_ps, b_ps, from_v=from_v)
@@ -1602,7 +1603,7 @@ def run_ours(args, cfg, rank, world, full=True):
                       "cta_rows": int(info.n_cta_rows), "cta_threshold": int(info.cta_threshold),
                       "l2": "cold before every timed step: persisting lines demoted "
                             "(cudaCtxResetPersistingL2Cache) then a 256 MiB write",
-                      "parallelism": (f"row-sharded x{world} (NCCL all-gather)" if sharded
+                      "parallelism": (f"row-sharded x{world} ({(args.dist_backend or 'nccl').upper()} all-gather)" if sharded
                                       else "1 GPU")},
             "l2_carveout": carve,
             "gat_form": ("layer: logits from the gathered V rows (GF_FLAG_LOGITS_FROM_V; Q, K = "
