@@ -47,6 +47,12 @@ namespace gfb {
 // order.  Measured per pass (profiles/r2/ab_r2_policy_param.txt): pairs help
 // pass B (-1.5 %) and the table-form pass A (-2 %), but cost the GAT
 // layer-form pass A 20 % (its 64-register budget), which keeps the sequence.
+#ifndef GF_BWD_LPH1
+#define GF_BWD_LPH1 0  // pass A, GAT layer-form warp rows with LPH = 1 at compile time: measured 12 % SLOWER (kept off)
+#endif
+#ifndef GF_BWDC_LPH1
+#define GF_BWDC_LPH1 1  // the same for pass B warp columns (C4 pass B -2.5 %)
+#endif
 #ifndef GF_BWD_DOT2
 #define GF_BWD_DOT2 1
 #endif
@@ -118,10 +124,11 @@ __device__ __forceinline__ void warp_sum(T (&x)[NV]) {
 }
 
 // ------------------------------------------------------------ pass A ------
-template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
+template <typename T, int CB, int LPE, int CPL, int VAR, bool PK, int LPHC = 0>
 __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
                                         const int nrows, const int4 ct) {
+  const int lph = LPHC ? LPHC : a.LPH;  // compile-time 1 for GAT layer-form warp rows (as fwd_row)
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -153,8 +160,8 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   if (r == 0 && !pk) nxt = eb + lane < ee ? ld_idx(a.idx + eb + lane) : 0;
   if constexpr (PKPRE) nxt = c < ee - eb ? ld_idx(a.idx + eb + c) : 0;
 
-  const int h = c / a.LPH;
-  const int off = h * a.D + (c % a.LPH) * NE;
+  const int h = c / lph;
+  const int off = h * a.D + (c % lph) * NE;
   const size_t vrow = static_cast<size_t>(v) * a.F + off;
   const size_t ri = static_cast<size_t>(v) * a.H + h;
   const T* __restrict__ Vb = a.V + off;
@@ -181,7 +188,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
     T s = T(0);
 #pragma unroll
     for (int i = 0; i < NE; ++i) s += dov[i] * ov[i];
-    delta = head_sum(s, a.LPH);
+    delta = head_sum(s, lph);
   }
   const Rec<T> rec = ld_rec(a.stats, ri);  // m, ll2 of this row; aux = er | 1/||K||
   T erv = T(0), rk = T(1);
@@ -241,18 +248,18 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           T dp = bdot<VAR != GF_ADDV>(dov, vv[t]);
-          dp = head_sum(dp, a.LPH);
+          dp = head_sum(dp, lph);
           T s, rq = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
             T d = bdot<true>(qv[t], kv), qq = bdot<true>(qv[t], qv[t]);
-            d = head_sum(d, a.LPH);
+            d = head_sum(d, lph);
             if (a.l2) {
-              rq = inv_norm(head_sum(qq, a.LPH));
+              rq = inv_norm(head_sum(qq, lph));
               d *= rq * rk;
             }
             s = a.scale * d;
           } else {
-            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), a.LPH);
+            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), lph);
             pre = el[t] + erv;
             s = lrelu(pre, a.slope);
           }
@@ -314,18 +321,18 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           T dp = bdot<VAR != GF_ADDV>(dov, vv[t]);
-          dp = head_sum(dp, a.LPH);
+          dp = head_sum(dp, lph);
           T s, rq = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
             T d = bdot<true>(qv[t], kv), qq = bdot<true>(qv[t], qv[t]);
-            d = head_sum(d, a.LPH);
+            d = head_sum(d, lph);
             if (a.l2) {
-              rq = inv_norm(head_sum(qq, a.LPH));
+              rq = inv_norm(head_sum(qq, lph));
               d *= rq * rk;
             }
             s = a.scale * d;
           } else {
-            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), a.LPH);
+            if constexpr (VAR == GF_ADDV) el[t] = head_sum(dot_n(vv[t], al), lph);
             pre = el[t] + erv;
             s = lrelu(pre, a.slope);
           }
@@ -362,14 +369,14 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   const bool writer = pk ? live : sub == 0;
 
   if constexpr (VAR == GF_DOT) {
-    if (a.l2) l2_backward_row<T, NE>(acc, kv, a.LPH);
+    if (a.l2) l2_backward_row<T, NE>(acc, kv, lph);
     if (writer) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k)
         st_chunk<T, CB>(a.dK + vrow + k * CW, *reinterpret_cast<T(*)[CW]>(acc + k * CW));
     }
   }
-  if (writer && c % a.LPH == 0) {
+  if (writer && c % lph == 0) {
     a.stats[4 * ri + 3] = delta;
     if constexpr (VAR != GF_DOT) a.dK[ri] = acc[0];
   }
@@ -390,8 +397,12 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {                              \
     const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;             \
     if (slot >= a.pk0) return;                                                                  \
-    ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, false, slot, true, min(a.rpw, a.pk0 - slot), \
-                                       one);                                                    \
+    if (GF_BWD_LPH1 && CPL == 1 && VAR == GF_ADDV && a.LPH == 1)                                \
+      ROWFN<T, CB, LPE, CPL, VAR, false, 1>(a, lane, warp, false, slot, true,                    \
+                                            min(a.rpw, a.pk0 - slot), one);                     \
+    else                                                                                        \
+      ROWFN<T, CB, LPE, CPL, VAR, false>(a, lane, warp, false, slot, true,                       \
+                                         min(a.rpw, a.pk0 - slot), one);                        \
   } else if constexpr (EPW > 1) {                                                               \
     const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +    \
                      lane / LPE;                                                                \
@@ -409,11 +420,12 @@ __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV ? GF_MINB_ROWS
 }
 
 // ------------------------------------------------------------ pass B ------
-template <typename T, int CB, int LPE, int CPL, int VAR, bool PK>
+template <typename T, int CB, int LPE, int CPL, int VAR, bool PK, int LPHC = 0>
 __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
                                         int /*nrows: pass B runs one column per warp, see below*/,
                                         const int4 ct) {
+  const int lph = LPHC ? LPHC : a.LPH;
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;
   constexpr int EPW = 32 / LPE;
@@ -437,8 +449,8 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
     split_range(sb, se, kWarpsPerBlock, warp, sb, se);
   }
 
-  const int h = c / a.LPH;
-  const int off = h * a.D + (c % a.LPH) * NE;
+  const int h = c / lph;
+  const int off = h * a.D + (c % lph) * NE;
   const size_t urow = static_cast<size_t>(u) * a.F + off;
   const T* __restrict__ dOb = a.dO + off;
   const uint32_t fb = a.F * sizeof(T);
@@ -460,14 +472,14 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
       T s = T(0);
 #pragma unroll
       for (int i = 0; i < NE; ++i) s += qu[i] * qu[i];
-      rq = inv_norm(head_sum(s, a.LPH));
+      rq = inv_norm(head_sum(s, lph));
     }
   } else if constexpr (VAR == GF_ADDV) {  // el = <V[u], a_l> from the owned V row
     T al[NE];
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       ld_own<T, CB>(a.Q + off + k * CW, *reinterpret_cast<T(*)[CW]>(al + k * CW));
-    elu = head_sum(dot_n(vu, al), a.LPH);
+    elu = head_sum(dot_n(vu, al), lph);
   } else {
     elu = __ldg(a.Q + static_cast<size_t>(u) * a.H + h);
   }
@@ -514,11 +526,11 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           T dp = bdot<true>(dov[t], vu);
-          dp = head_sum(dp, a.LPH);
+          dp = head_sum(dp, lph);
           T s, rk = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
             T d = bdot<true>(qu, kv[t]);
-            d = head_sum(d, a.LPH);
+            d = head_sum(d, lph);
             if (a.l2) {
               rk = rec[t].aux;
               d *= rq * rk;
@@ -586,11 +598,11 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           T dp = bdot<true>(dov[t], vu);
-          dp = head_sum(dp, a.LPH);
+          dp = head_sum(dp, lph);
           T s, rk = T(1), pre = T(0);
           if constexpr (VAR == GF_DOT) {
             T d = bdot<true>(qu, kv[t]);
-            d = head_sum(d, a.LPH);
+            d = head_sum(d, lph);
             if (a.l2) {
               rk = rec[t].aux;
               d *= rq * rk;
@@ -636,7 +648,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
   if constexpr (VAR == GF_DOT) {
 #pragma unroll
     for (int i = 0; i < NE; ++i) g[i] = all[NE + i];
-    if (a.l2) l2_backward_row<T, NE>(g, qu, a.LPH);
+    if (a.l2) l2_backward_row<T, NE>(g, qu, lph);
   }
   if (pk ? live : sub == 0) {
 #pragma unroll
@@ -646,7 +658,7 @@ __device__ __forceinline__ void bwd_col(const BwdArgs<T>& a, const int lane, con
         st_chunk<T, CB>(a.dQ + urow + k * CW, *reinterpret_cast<T(*)[CW]>(g + k * CW));
     }
     if constexpr (VAR != GF_DOT) {
-      if (c % a.LPH == 0) a.dQ[static_cast<size_t>(u) * a.H + h] = all[NE];
+      if (c % lph == 0) a.dQ[static_cast<size_t>(u) * a.H + h] = all[NE];
     }
   }
 }
@@ -667,7 +679,10 @@ __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_DOT ? GF_MINB_DOT1_
                          : (a.cta_tab ? __ldg(a.cta_tab + blockIdx.x) : make_int4(blockIdx.x, 0, 1, -1));
     const int slot = cta ? ct.x : a.n_cta + (blockIdx.x - cb) * kWarpsPerBlock + warp;
     if (!cta && slot >= a.pk0) return;
-    bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1, ct);
+    if (GF_BWDC_LPH1 && CPL == 1 && VAR == GF_ADDV && !cta && a.LPH == 1)
+      bwd_col<T, CB, LPE, CPL, VAR, false, 1>(a, lane, warp, false, slot, true, 1, ct);
+    else
+      bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1, ct);
   } else if constexpr (EPW > 1) {
     const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +
                      lane / LPE;

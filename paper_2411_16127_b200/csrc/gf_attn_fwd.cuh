@@ -37,6 +37,14 @@
 #define GF_WIDE_ADDR_FWD 1  // 1: V rows of the layer form / MODE 2-3 as one IMAD.WIDE.U32 (C4 fwd -1.5 %)
 #endif
 
+#ifndef GF_RESCALE_TH
+#define GF_RESCALE_TH 8  // natural-log units; 0 = rescale whenever a running max moves
+#endif
+
+#ifndef GF_FWD_LPH1
+#define GF_FWD_LPH1 1  // GAT layer-form warp rows with one lane per head: LPH = 1 at compile time
+#endif
+
 #ifndef GF_FWD_DOT2
 #define GF_FWD_DOT2 1
 #endif
@@ -73,10 +81,13 @@ __device__ __forceinline__ void merge_state(T& m, T& l, T (&acc)[N], T m2, T l2,
 // schedule entry two rows ahead and the next row's first 32 ids are loaded
 // while the current row's gathers are in flight, so consecutive rows do not
 // each pay the id round trip before their first gather.
-template <typename T, int CB, int LPE, int CPL, int VAR, int MODE, bool PK>
+template <typename T, int CB, int LPE, int CPL, int VAR, int MODE, bool PK, int LPHC = 0>
 __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, const int warp,
                                         const bool cta, const int slot, const bool live,
                                         const int nrows, const int4 ct) {
+  // lanes per head: compile-time for the hot one-lane-per-head rows (LPHC = 1:
+  // no head_sum loop guard and no reload of the runtime value per iteration)
+  const int lph = LPHC ? LPHC : a.LPH;
   constexpr int CW = Chunk<T, CB>::W;
   constexpr int NE = CPL * CW;  // elements per lane
   constexpr int EPW = 32 / LPE;
@@ -100,8 +111,8 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
   int4 rsn = GF_ROWPIPE && nrows > 1 ? ld_sched(a.sched + slot + 1) : zero4;
   int nxt = 0;
 
-  const int h = c / a.LPH;
-  const int off = h * a.D + (c % a.LPH) * NE;  // first element owned by this lane
+  const int h = c / lph;
+  const int off = h * a.D + (c % lph) * NE;  // first element owned by this lane
   const T* __restrict__ Vb = a.V + off;
   const T* __restrict__ Qb = a.Q + (VAR == GF_DOT ? off : h);
   const int qs = VAR == GF_DOT ? a.F : a.H;  // row stride of Q|el
@@ -144,7 +155,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       T s = T(0);
 #pragma unroll
       for (int i = 0; i < NE; ++i) s += kv[i] * kv[i];
-      rk = inv_norm(head_sum(s, a.LPH));
+      rk = inv_norm(head_sum(s, lph));
     }
     }
   } else if constexpr (is_addv(VAR)) {  // er = <V[v], a_r> from the row's own V
@@ -155,7 +166,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
                     *reinterpret_cast<T(*)[CW]>(vo + k * CW));
       ld_own<T, CB>(a.K + off + k * CW, *reinterpret_cast<T(*)[CW]>(ar + k * CW));
     }
-    erv = head_sum(dot_n(vo, ar), a.LPH);
+    erv = head_sum(dot_n(vo, ar), lph);
   } else {
     erv = __ldg(a.K + static_cast<size_t>(v) * a.H + h);
   }
@@ -236,19 +247,22 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
                 qq += qv[t][i] * qv[t][i];
               }
             }
-            d = head_sum(d, a.LPH);
-            if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
+            d = head_sum(d, lph);
+            if (a.l2) d *= inv_norm(head_sum(qq, lph)) * rk;
             s[t] = a.scale * d;
           } else if constexpr (is_addv(VAR)) {
-            s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
+            s[t] = lrelu(head_sum(dot_n(vv[t], al), lph) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
           }
           s[t] = ok[t] ? s[t] : ninf<T>();
           smax = GF_FMAX ? fmax(s[t], smax) : (s[t] > smax ? s[t] : smax);
         }
-        // Lazy rescale, warp-uniform: only when some lane's running max moves.
-        if (__any_sync(kFull, smax > m)) {
+        // Lazy rescale, warp-uniform: only when some lane's running max moves
+        // past m + GF_RESCALE_TH.  Below that the stale m is kept: p = e^(s-m)
+        // stays <= e^TH, and (m, l) remain a consistent pair (P = e^(s-m) / l
+        // for any m), so records, merges and the backward are unchanged.
+        if (__any_sync(kFull, smax > m + T(GF_RESCALE_TH))) {
           const T mn = smax > m ? smax : m;
           const T corr = m == mn ? T(1) : expd(m - mn);
           l *= corr;
@@ -337,19 +351,22 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
                 qq += qv[t][i] * qv[t][i];
               }
             }
-            d = head_sum(d, a.LPH);
-            if (a.l2) d *= inv_norm(head_sum(qq, a.LPH)) * rk;
+            d = head_sum(d, lph);
+            if (a.l2) d *= inv_norm(head_sum(qq, lph)) * rk;
             s[t] = a.scale * d;
           } else if constexpr (is_addv(VAR)) {
-            s[t] = lrelu(head_sum(dot_n(vv[t], al), a.LPH) + erv, a.slope);
+            s[t] = lrelu(head_sum(dot_n(vv[t], al), lph) + erv, a.slope);
           } else {
             s[t] = lrelu(s[t] + erv, a.slope);
           }
           s[t] = ok[t] ? s[t] : ninf<T>();
           smax = GF_FMAX ? fmax(s[t], smax) : (s[t] > smax ? s[t] : smax);
         }
-        // Lazy rescale, warp-uniform: only when some lane's running max moves.
-        if (__any_sync(kFull, smax > m)) {
+        // Lazy rescale, warp-uniform: only when some lane's running max moves
+        // past m + GF_RESCALE_TH.  Below that the stale m is kept: p = e^(s-m)
+        // stays <= e^TH, and (m, l) remain a consistent pair (P = e^(s-m) / l
+        // for any m), so records, merges and the backward are unchanged.
+        if (__any_sync(kFull, smax > m + T(GF_RESCALE_TH))) {
           const T mn = smax > m ? smax : m;
           const T corr = m == mn ? T(1) : expd(m - mn);
           l *= corr;
@@ -452,7 +469,7 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
       st_chunk<T, CB>(orow + k * CW, *reinterpret_cast<T(*)[CW]>(o + k * CW));
-    if (MODE < 2 && c % a.LPH == 0) {
+    if (MODE < 2 && c % lph == 0) {
       T* rec = a.stats + 4 * (static_cast<size_t>(v) * a.H + h);
       rec[0] = l == T(0) ? ninf<T>() : m;
       rec[1] = l == T(0) ? T(0) : lg2(l);
@@ -482,8 +499,12 @@ __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_MINB_
   } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {
     const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;
     if (slot >= a.pk0) return;
-    fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, false, slot, true,
-                                               min(a.rpw, a.pk0 - slot), one);
+    if (GF_FWD_LPH1 && CPL == 1 && is_addv(VAR) && a.LPH == 1)  // (table form: measured slower)
+      fwd_row<T, CB, LPE, CPL, VAR, MODE, false, 1>(a, lane, warp, false, slot, true,
+                                                    min(a.rpw, a.pk0 - slot), one);
+    else
+      fwd_row<T, CB, LPE, CPL, VAR, MODE, false>(a, lane, warp, false, slot, true,
+                                                 min(a.rpw, a.pk0 - slot), one);
   } else if constexpr (EPW > 1) {
     const int slot = a.pk0 + ((blockIdx.x - cb - a.wblocks) * kWarpsPerBlock + warp) * EPW +
                      lane / LPE;
