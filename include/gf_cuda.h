@@ -22,8 +22,10 @@
  *   dot: Q, K, dQ, dK are N x (H*D); add: el, er, del, der are N x H;
  *   V, O, dO, dV are N x (H*D); all row-major, element type `dtype`.
  *   stats is N x H x 4 softmax records {m, log2 l, aux, delta} per (row,
- *   head): m = row max of the scores, l = sum exp(s - m) (so p is recomputed
- *   as exp((s - m) - log l) with full relative precision for any |s|),
+ *   head): m = a reference score at most 8 below the row max (the forward
+ *   rescales its running sum lazily), l = sum exp(s - m) (so p is recomputed
+ *   as exp((s - m) - log l) with full relative precision for any |s|; only
+ *   the pair is meaningful, m + ln(2) log2 l = the row's log-sum-exp),
  *   aux = er (GAT) or 1/max(||K||, eps) (AGNN), delta = <dO, O> (written by
  *   backward pass A).  Base pointers must be 32-byte aligned for the 256-bit
  *   gather path (torch / cudaMalloc allocations are); other alignments fall

@@ -366,7 +366,8 @@ __device__ __forceinline__ T ninf() {
 // ------------------------------------------------------ softmax records --
 // Per (row v, head h) record of 4 T, written by the forward and pass A and
 // gathered by pass B in ONE load:
-//   [0] m     row max of the scores (natural units)
+//   [0] m     reference score (natural units): the row max up to the
+//             forward's lazy-rescale threshold (m >= max - GF_RESCALE_TH)
 //   [1] ll2   log2 of l = sum exp(s - m)        => p = 2^((s - m) log2e - ll2)
 //   [2] aux   er[v,h] (GAT) | 1/max(||K[v,h]||,eps) (AGNN) | 0
 //   [3] delta <dO[v,h], O[v,h]> (written by backward pass A)

@@ -113,8 +113,9 @@ def test_source_phased_forward(cuda, world, cfg):
     """The overlapped forward (shard.source_parts / phase_forward /
     merge_phases): every simulated rank runs one forward per source block
     (own block first) into row-block partials and merges them.  O and the
-    records match the one-pass forward within fp32 rounding (the row max m
-    and aux exactly); the backward on the merged records matches too."""
+    records match the one-pass forward within fp32 rounding (the log-sum-exp
+    of the (m, log2 l) pair; aux exactly); the backward on the merged records
+    matches too."""
     from paper_2411_16127_b200 import fused
     from paper_2411_16127_b200.shard import (RowShard, merge_phases, part_buffers, phase_forward,
                                              phase_order, source_parts)
@@ -150,9 +151,11 @@ def test_source_phased_forward(cuda, world, cfg):
     O2, st2 = s0.from_padded(Op), s0.from_padded(stp)
     nz = torch.from_numpy(np.diff(g.row_ptr) > 0).to(cuda)
     assert float((O2 - O1).abs().max()) <= 2e-6 * max(1.0, float(O1.abs().max()))
-    assert torch.equal(st2[nz][..., 0], st1[nz][..., 0])  # row max
+    # (m, log2 l) is a consistent pair, not unique: the forward keeps a stale
+    # m within GF_RESCALE_TH of the row max, so compare the log-sum-exp
+    lse1, lse2 = fused.lse_of(st1)[nz], fused.lse_of(st2)[nz]
+    assert float((lse2 - lse1).abs().max()) <= 1e-5 * max(1.0, float(lse1.abs().max()))
     assert torch.equal(st2[nz][..., 2], st1[nz][..., 2])  # aux (er | 1/||K||)
-    assert float((st2[nz][..., 1] - st1[nz][..., 1]).abs().max()) <= 1e-5
     # backward on the merged records (one-pass shard graphs)
     dQp, dKp, dVp = torch.zeros_like(Qp), torch.zeros_like(Kp), torch.zeros_like(Vp)
     graphs = [sh.device_graph(cta_threshold=64) for sh in shards]
