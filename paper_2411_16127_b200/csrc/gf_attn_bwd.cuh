@@ -48,7 +48,7 @@ namespace gfb {
 // pass B (-1.5 %) and the table-form pass A (-2 %), but cost the GAT
 // layer-form pass A 20 % (its 64-register budget), which keeps the sequence.
 #ifndef GF_BWD_LPH1
-#define GF_BWD_LPH1 0  // pass A, GAT layer-form warp rows with LPH = 1 at compile time: measured 12 % SLOWER (kept off)
+#define GF_BWD_LPH1 1  // pass A, GAT layer-form warp rows with LPH = 1 at compile time
 #endif
 #ifndef GF_BWDC_LPH1
 #define GF_BWDC_LPH1 1  // the same for pass B warp columns (C4 pass B -2.5 %)
@@ -225,13 +225,21 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
       for (int j0 = jb; j0 < je; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], el[U];
+        int uus[U];
+        // every slot's id first, then every gather: without the head_sum
+        // branches (LPHC = 1) ptxas otherwise starts slot 0's math before
+        // issuing slot 1's load, serialising the two L2 round trips
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
           const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
                         : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-          const int uu = ok[t] ? u : 0;
+          uus[t] = ok[t] ? u : 0;
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int uu = uus[t];
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
@@ -298,13 +306,21 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
       for (int j0 = 0; j0 < cntw; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], el[U];
+        int uus[U];
+        // every slot's id first, then every gather: without the head_sum
+        // branches (LPHC = 1) ptxas otherwise starts slot 0's math before
+        // issuing slot 1's load, serialising the two L2 round trips
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;
           const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
                         : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-          const int uu = ok[t] ? u : 0;
+          uus[t] = ok[t] ? u : 0;
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int uu = uus[t];
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>(row_at(Vb, uu, fb) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
