@@ -45,6 +45,10 @@
 #define GF_FWD_LPH1 1  // GAT layer-form warp rows with one lane per head: LPH = 1 at compile time
 #endif
 
+#ifndef GF_FWD_LPH1_TABLE
+#define GF_FWD_LPH1_TABLE 0  // the same for the el / er table form (measured 6 % slower before the id hoist)
+#endif
+
 #ifndef GF_FWD_DOT2
 #define GF_FWD_DOT2 1
 #endif
@@ -198,13 +202,21 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       for (int j0 = jb; j0 < je; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], s[U];
+        int uus[U];
+        // every slot's id before any gather (as pass A: keeps ptxas from
+        // starting slot 0's math ahead of the later slots' loads)
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
           const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
                         : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-          const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+          uus[t] = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          const int uu = uus[t];
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>((WIDE ? row_at(Vb, uu, fb) : Vb + uu * a.F) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
@@ -302,13 +314,21 @@ __device__ __forceinline__ void fwd_row(const FwdArgs<T>& a, const int lane, con
       for (int j0 = 0; j0 < cntw; j0 += ep * U) {
         bool ok[U];
         T vv[U][NE], qv[U][NE], s[U];
+        int uus[U];
+        // every slot's id before any gather (as pass A: keeps ptxas from
+        // starting slot 0's math ahead of the later slots' loads)
   #pragma unroll
         for (int t = 0; t < U; ++t) {
           const int j = j0 + t * ep + js;
           ok[t] = FULL || j < cnt;  // FULL: a whole 32-edge chunk, no masks
           const int u = PKPRE ? __shfl_sync(kFull, myu, (lane & ~(LPE - 1)) + (j & (LPE - 1)))
                         : pk ? (ok[t] ? ld_idx(a.idx + base + j) : 0) : __shfl_sync(kFull, myu, j & 31);
-          const int uu = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+          uus[t] = ok[t] ? u : 0;  // in-range dummy row for masked lanes
+        }
+  #pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int j = j0 + t * ep + js;
+          const int uu = uus[t];
   #pragma unroll
           for (int k = 0; k < CPL; ++k)
             ld_gather<T, CB>((WIDE ? row_at(Vb, uu, fb) : Vb + uu * a.F) + k * CW, *reinterpret_cast<T(*)[CW]>(vv[t] + k * CW), pol);
@@ -499,7 +519,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_ADDV_HBM ? GF_MINB_
   } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {
     const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;
     if (slot >= a.pk0) return;
-    if (GF_FWD_LPH1 && CPL == 1 && is_addv(VAR) && a.LPH == 1)  // (table form: measured slower)
+    if (GF_FWD_LPH1 && CPL == 1 && (is_addv(VAR) || (GF_FWD_LPH1_TABLE && VAR == GF_ADD)) && a.LPH == 1)
       fwd_row<T, CB, LPE, CPL, VAR, MODE, false, 1>(a, lane, warp, false, slot, true,
                                                     min(a.rpw, a.pk0 - slot), one);
     else
