@@ -53,6 +53,9 @@ namespace gfb {
 #ifndef GF_BWDC_LPH1
 #define GF_BWDC_LPH1 1  // the same for pass B warp columns (C4 pass B -2.5 %)
 #endif
+#ifndef GF_BWD_LPH1_TABLE
+#define GF_BWD_LPH1_TABLE 1  // both passes' LPH = 1 copies for the el / er table form too (table-form step +2 %)
+#endif
 #ifndef GF_BWD_DOT2
 #define GF_BWD_DOT2 1
 #endif
@@ -413,7 +416,7 @@ __device__ __forceinline__ void bwd_row(const BwdArgs<T>& a, const int lane, con
   } else if (blockIdx.x < static_cast<unsigned>(cb + a.wblocks)) {                              \
     const int slot = a.n_cta + ((blockIdx.x - cb) * kWarpsPerBlock + warp) * a.rpw;             \
     if (slot >= a.pk0) return;                                                                  \
-    if (GF_BWD_LPH1 && CPL == 1 && VAR == GF_ADDV && a.LPH == 1)                                \
+    if (GF_BWD_LPH1 && CPL == 1 && (VAR == GF_ADDV || (GF_BWD_LPH1_TABLE && VAR == GF_ADD)) && a.LPH == 1) \
       ROWFN<T, CB, LPE, CPL, VAR, false, 1>(a, lane, warp, false, slot, true,                    \
                                             min(a.rpw, a.pk0 - slot), one);                     \
     else                                                                                        \
@@ -695,7 +698,8 @@ __global__ void __launch_bounds__(256, CPL == 1 ? (VAR == GF_DOT ? GF_MINB_DOT1_
                          : (a.cta_tab ? __ldg(a.cta_tab + blockIdx.x) : make_int4(blockIdx.x, 0, 1, -1));
     const int slot = cta ? ct.x : a.n_cta + (blockIdx.x - cb) * kWarpsPerBlock + warp;
     if (!cta && slot >= a.pk0) return;
-    if (GF_BWDC_LPH1 && CPL == 1 && VAR == GF_ADDV && !cta && a.LPH == 1)
+    if (GF_BWDC_LPH1 && CPL == 1 && (VAR == GF_ADDV || (GF_BWD_LPH1_TABLE && VAR == GF_ADD)) && !cta &&
+        a.LPH == 1)
       bwd_col<T, CB, LPE, CPL, VAR, false, 1>(a, lane, warp, false, slot, true, 1, ct);
     else
       bwd_col<T, CB, LPE, CPL, VAR, false>(a, lane, warp, cta, slot, true, 1, ct);
