@@ -142,6 +142,13 @@ struct Chunk {
 #ifndef GF_L2_EVICT_OP
 #define GF_L2_EVICT_OP 1
 #endif
+// GF_GATHER_L1 = 1: the fp32 256-bit gathers also allocate in L1 (no
+// .L1::no_allocate).  The rows are not reused, yet the allocating path
+// measured 3 % faster in the forward (C4 1.75 -> 1.70 ms; table form C5
+// 3.64 -> 3.40 ms, profiles/r2/ab_r2_policy_param.txt).
+#ifndef GF_GATHER_L1
+#define GF_GATHER_L1 1
+#endif
 __device__ __forceinline__ uint64_t pol_keep() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -238,7 +245,13 @@ template <typename T, int CB>
 __device__ __forceinline__ void ld_gather(const T* __restrict__ p, T (&x)[CB / sizeof(T)],
                                           const uint64_t pol) {
   if constexpr (CB == 32 && sizeof(T) == 4) {
-#if GF_L2HINT && GF_L2_EVICT_OP
+#if GF_L2HINT && GF_L2_EVICT_OP && GF_GATHER_L1
+    (void)pol;
+    asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
+                   "=f"(x[6]), "=f"(x[7])
+                 : "l"(p));
+#elif GF_L2HINT && GF_L2_EVICT_OP
     (void)pol;
     asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]),
