@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2411_16127_b200", "libgraphfuse_cuda.so")
 KEYS = ("UTCHMMA", "UTCQMMA", "UTMALDG", "UTMASTG", "UTMAREDG", "LDTM", "STTM",
-        "LDG.E.NA.ELL2.256", "LDG.E.NA.ENL2.256", "LDG.E.ENL2.256", "FFMA2", "FMUL2",
+        "LDG.E.NA.ELL2.256", "LDG.E.ELL2.256", "LDG.E.NA.ENL2.256", "LDG.E.ENL2.256", "FFMA2", "FMUL2",
         "MUFU.EX2", "STL", "LDL", "R2UR")
 # the C4 layer-form kernels (GAT 8x8 fp32: CB 32, LPE 8, CPL 1, VAR GF_ADDV)
 MAIN = ("fwd_fastIfLi32ELi8ELi1ELi2ELi0E", "bwd_rows_fastIfLi32ELi8ELi1ELi2E",
